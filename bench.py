@@ -1,0 +1,424 @@
+"""Benchmark of the TrackerSplat motion-estimation hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+A step is one frame pair through the whole hot path: K1 projection + depth order + tile binning,
+K2 fused raster-accumulate, K3 per-(view, Gaussian) affine fit, K4 multi-view fuse -- the four
+★ stages of compensate_frame (pipeline.py:117-124, :79-86).  Workload (BASELINE.json configs[1]):
+300k Gaussians, 20 views of 1352x1014, synthetic scene from generate_scene(seed 0, focal 1200),
+dense tracks from the GPU oracle tracker (sigma 0).
+
+metric: Gaussian-views/s of the motion fit (N*V per step / step time, whole job over all ranks).
+value: device time with inputs resident in HBM (CUDA events on the launch stream, max over ranks).
+e2e: the same through the public engine API with HOST inputs: pinned H2D of Gaussians + tracks and
+     D2H of the updates inside every timed step.
+roofline: K2 (the dominant kernel) achieved algorithmic bytes / its CUDA-event launch time vs the
+     measured HBM copy bandwidth.  B_K2 = 9*V*W*H + 96*N*V.
+cpu_baseline: the CPU oracle port (oracle/: C raster/accumulate, numpy/LAPACK solve and fuse) on a
+     bounded sample, in a process pool over all host cores.
+--impl reference: the same CPU port as the reference arm, timed per step on a bounded sample.
+Multi-GPU (torchrun): weak scaling, one target frame per rank (short-clip frame sharding,
+pipeline.py:64-65): Gaussians broadcast from rank 0 once per clip over NCCL, updated Gaussians
+gathered to rank 0 over NCCL inside each step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(args=(1, 10_000, 4), kw=dict(focal=180, width=128, height=128,
+                                              scale_range=(0.01, 0.02)), gap=1,
+                 name="synthetic rigid-motion scene: 10k Gaussians, 4 views 128x128"),
+    "cfg2": dict(args=(0, 300_000, 20), kw=dict(focal=1200, width=1352, height=1014), gap=1,
+                 name="N3DV-scale synthetic: 300k Gaussians, 20 views 1352x1014, one frame pair"),
+    "cfg3": dict(args=(0, 200_000, 27), kw=dict(focal=520, width=640, height=360,
+                                                translate_mag=0.12, rotate_deg=3.0), gap=6,
+                 name="Panoptic-scale large displacement: 200k Gaussians, 27 views 640x360, "
+                      "6-frame gap"),
+    "cfg4": dict(args=(0, 500_000, 20), kw=dict(focal=1100, width=1352, height=1014), gap=1,
+                 name="multi-frame parallel: 500k Gaussians, 20 views 1352x1014, one frame per GPU"),
+}
+METRIC = "Gaussian-views/sec motion-fit"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0
+LAUNCHES_PER_STEP = 22  # our kernels per frame incl. CUB passes (profiles/ launch list)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# inputs
+
+def make_inputs(cfgname, n_frames, log_prefix=""):
+    """Scene (host arrays) + dense tracks for frames 1..n_frames-1 (GPU tensors)."""
+    import torch
+
+    from paper_2604_02586_b200.engine import FrameEngine
+    from paper_2604_02586_b200.scene import generate_scene, oracle_tracks
+    c = CONFIGS[cfgname]
+    seed, n, v = c["args"]
+    t0 = time.time()
+    scene = generate_scene(seed, n, v, n_frames, **c["kw"])
+    log(f"{log_prefix}scene {cfgname}: N={n} V={v} frames={n_frames} in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    eng = FrameEngine().bin(scene.frames[0], scene.cameras)
+    tracks = {}
+    for f in range(1, n_frames):
+        tracks[f] = oracle_tracks(scene, f, engine=eng)
+    torch.cuda.synchronize()
+    log(f"{log_prefix}tracks in {time.time() - t0:.1f}s")
+    return scene, tracks
+
+
+def k2_bytes(n, v, w, h):
+    return 9 * v * w * h + 96 * n * v
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample)
+
+def _cpu_view_task(args):
+    g, cam, target, valid = args
+    import oracle
+    t0 = time.perf_counter()
+    wm = oracle.rasterize(g, cam)
+    acc = oracle.accumulate(wm, target, valid, len(g))
+    sv = oracle.solve_view(acc)
+    return time.perf_counter() - t0, sv
+
+
+def cpu_baseline(scene, tracks, frame, n_views_sample, n_fuse_sample, procs):
+    """Time the oracle's ★ stages on a bounded sample: raster+accumulate+solve for
+    `n_views_sample` full views (process pool over views), update_all on `n_fuse_sample`
+    Gaussians; extrapolate to the full frame."""
+    import multiprocessing as mp
+
+    import oracle
+    oracle._lib()
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    g = scene.frames[0]
+    n = len(g)
+    cams = np.array([c.as_row() for c in scene.cameras])
+    nv = len(cams)
+    tgt, val = tracks[frame]
+    views = list(range(min(n_views_sample, nv)))
+    tasks = [(g, cams[v], tgt[v].cpu().numpy().astype(np.float64),
+              val[v].cpu().numpy().astype(bool)) for v in views]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(min(procs, len(tasks))) as pool:
+        res = pool.map(_cpu_view_task, tasks)
+    t_views = time.perf_counter() - t0
+    per_view = float(np.mean([r[0] for r in res]))
+    # fuse sample: all views' motions are needed; reuse sampled views' motions cyclically
+    sv = [r[1] for r in res]
+    mot = {k: np.stack([sv[v % len(sv)][k] for v in range(nv)]) for k in
+           ("status", "a", "b", "weight_sum", "pixel_count")}
+    idx = np.arange(min(n_fuse_sample, n))
+    sub = {k: mot[k][:, idx] for k in mot}
+    t0 = time.perf_counter()
+    oracle.update_all(g[idx], sub, cams)
+    t_fuse = (time.perf_counter() - t0) * (n / len(idx))
+    # full-frame single-process-equivalent times, and the pooled wall rate
+    cores = min(procs, len(tasks))
+    t_motion_wall = per_view * nv / cores
+    gv_s = n * nv / t_motion_wall
+    frames_s = 1.0 / (t_motion_wall + t_fuse / cores)
+    sample = (f"{len(views)} of {nv} views raster+accumulate+solve in full "
+              f"({per_view:.2f}s/view single-process, {cores} processes, pool wall "
+              f"{t_views:.1f}s), update_all on {len(idx)} of {n} Gaussians extrapolated")
+    return dict(value=gv_s, frames_per_s=frames_s, cores=cores, sample=sample,
+                t_view_s=per_view, t_fuse_frame_s=t_fuse)
+
+
+# ---------------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02586_b200.engine import FrameEngine
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.config]
+    seed, n, nv = c["args"]
+    gap = c["gap"]
+    frame = gap * (rank + 1)
+    # every rank regenerates the (deterministic) scene; frame-0 Gaussians are then broadcast
+    # from rank 0 over NCCL (once per clip), tracks are rank-local
+    scene, tracks = make_inputs(args.config, gap * world + 1, f"[rank {rank}] ")
+    w, h = scene.cameras[0].width, scene.cameras[0].height
+    dev = torch.device("cuda", local)
+    g_dev = torch.as_tensor(scene.frames[0], device=dev)
+    if world > 1:
+        dist.broadcast(g_dev, 0)
+    tgt, val = tracks[frame]
+    cams = scene.cameras
+    eng = FrameEngine()
+    stream = torch.cuda.current_stream()
+
+    def step(out=None):
+        eng.bin(g_dev, cams)
+        return eng.compensate(tgt, val, out)
+
+    out = None
+    for _ in range(args.warmup):
+        out = step(out)
+    torch.cuda.synchronize()
+    gather_buf = None
+    if world > 1:
+        gather_buf = [torch.empty((n, 11), dtype=torch.float64, device=dev) for _ in range(world)]
+
+    def updated_rows(o):
+        rows = g_dev.clone()
+        keep = o.status != 0
+        rows[keep, 0:3] += o.delta_mean[keep]
+        rows[keep, 3:7] = o.rotation[keep]
+        rows[keep, 7:10] = o.scale[keep]
+        return rows
+
+    eng.plan.timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            out = step(out)
+            if world > 1:
+                dist.gather(updated_rows(out), gather_buf if rank == 0 else None, dst=0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stages = eng.plan.timing_read()
+    eng.plan.timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n * nv * world / (ms / 1e3)
+
+    # e2e through the public engine API with pinned HOST inputs and a host read of the result
+    g_host = torch.from_numpy(np.ascontiguousarray(scene.frames[0])).pin_memory()
+    t_host = tgt.cpu().pin_memory()
+    v_host = val.cpu().pin_memory()
+    eng2 = FrameEngine(eng.plan)
+    d_out = None
+    res_host = None
+
+    def e2e_step():
+        nonlocal d_out, res_host
+        g_d = g_host.to(dev, non_blocking=True)
+        t_d = t_host.to(dev, non_blocking=True)
+        v_d = v_host.to(dev, non_blocking=True)
+        eng2.bin(g_d, cams)
+        d_out = eng2.compensate(t_d, v_d, d_out)
+        res = torch.cat([d_out.delta_mean, d_out.rotation, d_out.scale,
+                         d_out.status.to(torch.float64)[:, None]], 1)
+        res_host = res.to("cpu")
+        return res_host
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = g_host.numel() * 8 + t_host.numel() * 4 + v_host.numel()
+    d2h = res_host.numel() * 8
+
+    line = None
+    if rank == 0:
+        k2_ms = stages["k2_raster_accumulate"][0] / max(stages["k2_raster_accumulate"][1], 1)
+        peak, peak_kind = hbm_peak()
+        bk2 = k2_bytes(n, nv, w, h)
+        achieved = bk2 / (k2_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"k2_traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        stage_ms = {k: round(v[0] / max(v[1], 1), 4) for k, v in stages.items()}
+        tallies = out.tallies()
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cb = cpu_baseline(scene, {frame: (tgt, val)}, frame, args.cpu_views,
+                              args.cpu_fuse, len(os.sched_getaffinity(0)))
+            cpu = {"value": cb["value"], "unit": "Gaussian-views/s", "cores": cb["cores"],
+                   "kind": "port", "sample": cb["sample"],
+                   "frames_per_s": cb["frames_per_s"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gaussian-views/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
+            "config": {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w,
+                       "height": h, "target_frame_per_rank": "gap*(rank+1)",
+                       "frames_per_s": world / (ms / 1e3),
+                       "parallelism": f"frame-sharded x{world}",
+                       "l2": "working set (tracks 247 MB, records 384 MB) exceeds the 126 MB L2"},
+            "e2e": {"value": n * nv * world / (ms_e2e / 1e3), "unit": "Gaussian-views/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": ms_e2e},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k2_raster_accumulate", "algorithmic_bytes": bk2,
+                         "kernel_ms": k2_ms, "peak_kind": peak_kind},
+            "stage_ms": stage_ms, "tallies": tallies,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def run_reference(args):
+    """Reference arm: the CPU port of the reference algorithm (oracle/), all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import torch
+    c = CONFIGS[args.config]
+    seed, n, nv = c["args"]
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    scene, tracks = make_inputs(args.config, c["gap"] + 1)
+    frame = c["gap"]
+    procs = len(os.sched_getaffinity(0))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(scene, tracks, frame, args.cpu_views, args.cpu_fuse, procs)
+        if i >= args.warmup:
+            vals.append(cb)
+    value = float(np.mean([v["value"] for v in vals]))
+    ms = n * nv / value * 1e3
+    w, h = scene.cameras[0].width, scene.cameras[0].height
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gaussian-views/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
+            "config": {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w,
+                       "height": h},
+            "cpu_baseline": {"value": value, "unit": "Gaussian-views/s",
+                             "cores": vals[-1]["cores"], "kind": "port",
+                             "sample": vals[-1]["sample"]},
+            "e2e": {"value": value, "unit": "Gaussian-views/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-views", type=int, default=8)
+    ap.add_argument("--cpu-fuse", type=int, default=3000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,667 @@
+// api.cu -- C ABI of the B200 hot path: plan (device workspace), K1..K4 orchestration, CUB sorts.
+//
+// Everything is stream-ordered on the caller's stream; the plan owns a grow-only device workspace
+// allocated with cudaMallocAsync.  The only host synchronisations are the data-dependent sizes
+// (instance count after binning, contribution count of the emitting rasterizer).
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace ts;
+
+namespace {
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need, cudaStream_t s) {
+    if (need <= bytes && p) return cudaSuccess;
+    if (p) {
+      cudaError_t e = cudaFreeAsync(p, s);
+      if (e != cudaSuccess) return e;
+      p = nullptr;
+      bytes = 0;
+    }
+    size_t want = need + need / 4 + 256;
+    cudaError_t e = cudaMallocAsync(&p, want, s);
+    if (e != cudaSuccess) return e;
+    bytes = want;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+int bits_for(uint64_t x) {  // number of bits needed to represent values < x
+  int b = 0;
+  while (b < 64 && (1ull << b) < x) b++;
+  return b < 1 ? 1 : b;
+}
+
+enum Stage { ST_PROJECT = 0, ST_DEPTH_SORT, ST_TILE_SORT, ST_RASTER, ST_SOLVE, ST_FUSE, ST_N };
+
+}  // namespace
+
+struct ts_plan {
+  // binning state
+  DevBuf cams, rec, dkey, dkey2, dval, dval2, depth64, ntiles, status, bbox, cnt_sorted, off_sorted,
+      inst_base, tkey, tkey2, tval, tval2, range, cub_tmp;
+  // per-frame state
+  DevBuf partial, flag, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt, mot_sw;
+  // stage-API buffers
+  DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
+      deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
+  uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
+  int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
+  int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
+  const double *gaussians = nullptr;
+  std::vector<ts_camera> host_cams;
+  ts_config cfg{};
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks;
+  size_t ev_next = 0;
+
+  cudaEvent_t take_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
+  cudaEvent_t mark_begin(cudaStream_t s) {
+    if (!timing) return nullptr;
+    cudaEvent_t e = take_event();
+    cudaEventRecord(e, s);
+    return e;
+  }
+  void mark_end(int stage, cudaEvent_t b, cudaStream_t s) {
+    if (!timing || !b) return;
+    cudaEvent_t e = take_event();
+    cudaEventRecord(e, s);
+    ev_marks.push_back({stage, {b, e}});
+  }
+  DevBuf *all_bufs() { return &cams; }
+};
+
+namespace {
+
+template <typename T>
+T *ptr(DevBuf &b) { return b.as<T>(); }
+
+#define ENSURE(buf, bytes) TS_CUDA_TRY((buf).ensure((size_t)(bytes), s))
+
+int64_t sum_workspace(const ts_plan *p) {
+  const DevBuf *bufs[] = {&p->cams, &p->rec, &p->dkey, &p->dkey2, &p->dval, &p->dval2, &p->depth64,
+                          &p->ntiles, &p->status, &p->bbox, &p->cnt_sorted, &p->off_sorted,
+                          &p->inst_base, &p->tkey, &p->tkey2, &p->tval, &p->tval2, &p->range,
+                          &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a,
+                          &p->mot_b, &p->mot_w, &p->mot_cnt, &p->mot_scnt, &p->mot_sw,
+                          &p->emit_count, &p->emit_key, &p->emit_key2, &p->emit_gv,
+                          &p->emit_alpha, &p->emit_trans, &p->emit_idx, &p->emit_idx2,
+                          &p->deg_flags, &p->deg_ids, &p->deg_count, &p->acc_keys, &p->acc_keys2,
+                          &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end};
+  int64_t t = 0;
+  for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
+  return t;
+}
+
+void release_all(ts_plan *p) {
+  DevBuf *bufs[] = {&p->cams, &p->rec, &p->dkey, &p->dkey2, &p->dval, &p->dval2, &p->depth64,
+                    &p->ntiles, &p->status, &p->bbox, &p->cnt_sorted, &p->off_sorted,
+                    &p->inst_base, &p->tkey, &p->tkey2, &p->tval, &p->tval2, &p->range,
+                    &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a, &p->mot_b,
+                    &p->mot_w, &p->mot_cnt, &p->mot_scnt, &p->mot_sw, &p->emit_count,
+                    &p->emit_key, &p->emit_key2, &p->emit_gv, &p->emit_alpha, &p->emit_trans,
+                    &p->emit_idx, &p->emit_idx2, &p->deg_flags, &p->deg_ids, &p->deg_count,
+                    &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
+                    &p->seg_end};
+  for (DevBuf *b : bufs) b->release();
+}
+
+__global__ void k_iota(uint32_t *x, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (uint32_t)i;
+}
+__global__ void k_gid_keys(const int64_t *gid, uint32_t *keys, int64_t m) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) keys[i] = (uint32_t)gid[i];
+}
+__global__ void k_degenerate_flags(const int8_t *status, int64_t n, uint8_t *flags) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = status[i] == 1;
+}
+__global__ void k_fetch_contribs(const uint64_t *key_sorted, const uint32_t *idx_sorted,
+                                 const uint32_t *emit_gv, const double *emit_alpha,
+                                 const double *emit_trans, const RasterRec *rec,
+                                 const double *depth64, int64_t m, int W, int32_t *px,
+                                 int32_t *py, int64_t *gid, double *alpha, double *trans,
+                                 double *depth) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t k = idx_sorted[i];
+  const uint32_t pix = (uint32_t)(key_sorted[i] >> 32);
+  const uint32_t gv = emit_gv[k];
+  px[i] = (int32_t)(pix % (uint32_t)W);
+  py[i] = (int32_t)(pix / (uint32_t)W);
+  gid[i] = (int64_t)rec[gv].g;
+  alpha[i] = emit_alpha[k];
+  trans[i] = emit_trans[k];
+  depth[i] = depth64[gv];
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <typename F>
+cudaError_t cub_call(ts_plan *p, cudaStream_t s, F f) {
+  size_t need = 0;
+  cudaError_t e = f((void *)nullptr, need);
+  if (e != cudaSuccess) return e;
+  e = p->cub_tmp.ensure(need, s);
+  if (e != cudaSuccess) return e;
+  size_t have = p->cub_tmp.bytes;
+  return f(p->cub_tmp.p, have);
+}
+
+int validate_cams(const ts_camera *cams, int V) {
+  if (!cams || V < 1) return TS_E_INVALID_ARGUMENT;
+  for (int v = 0; v < V; v++) {
+    if (cams[v].width <= 0 || cams[v].height <= 0 || cams[v].width > 32767 ||
+        cams[v].height > 32767)
+      return TS_E_INVALID_ARGUMENT;
+    if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+      return TS_E_DIMENSION_MISMATCH;
+  }
+  return TS_OK;
+}
+
+// K1 + sorts + ranges into the plan.
+int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int V,
+              const ts_config *cfg, cudaStream_t s) {
+  int rc = validate_cams(cams, V);
+  if (rc) return rc;
+  if (n < 0 || (uint64_t)n * (uint64_t)V >= 0xFFFFFFFFull) return TS_E_INVALID_ARGUMENT;
+  p->n = n;
+  p->V = V;
+  p->W = cams[0].width;
+  p->H = cams[0].height;
+  p->tiles_x = (p->W + TS_TILE - 1) / TS_TILE;
+  p->tiles_y = (p->H + TS_TILE - 1) / TS_TILE;
+  p->tpv = p->tiles_x * p->tiles_y;
+  p->gaussians = G;
+  p->host_cams.assign(cams, cams + V);
+  if (cfg) p->cfg = *cfg;
+  const int64_t NV = n * V;
+  if (!p->host_small) TS_CUDA_TRY(cudaMallocHost(&p->host_small, 64));
+
+  ENSURE(p->cams, sizeof(ts_camera) * V);
+  TS_CUDA_TRY(cudaMemcpyAsync(p->cams.p, cams, sizeof(ts_camera) * V, cudaMemcpyHostToDevice, s));
+  ENSURE(p->rec, sizeof(RasterRec) * NV);
+  ENSURE(p->dkey, 8 * NV);
+  ENSURE(p->dkey2, 8 * NV);
+  ENSURE(p->dval, 4 * NV);
+  ENSURE(p->dval2, 4 * NV);
+  ENSURE(p->depth64, 8 * NV);
+  ENSURE(p->ntiles, 4 * NV);
+  ENSURE(p->status, NV);
+  ENSURE(p->bbox, 8 * NV);
+  ENSURE(p->cnt_sorted, 4 * NV);
+  ENSURE(p->off_sorted, 4 * NV);
+  ENSURE(p->inst_base, 4 * NV);
+  const int64_t ntile_total = (int64_t)p->tpv * V;
+  ENSURE(p->range, 8 * ntile_total);
+
+  cudaEvent_t e0 = p->mark_begin(s);
+  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec), ptr<uint64_t>(p->dkey),
+                    ptr<uint32_t>(p->dval), ptr<double>(p->depth64), ptr<uint32_t>(p->ntiles),
+                    ptr<int8_t>(p->status), ptr<int16_t>(p->bbox), s);
+  TS_CUDA_TRY(cudaGetLastError());
+  p->mark_end(ST_PROJECT, e0, s);
+
+  cudaEvent_t e1 = p->mark_begin(s);
+  if (NV > 0) {
+    const int end_bit = 32 + bits_for((uint64_t)V);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint64_t>(p->dkey),
+                                             ptr<uint64_t>(p->dkey2), ptr<uint32_t>(p->dval),
+                                             ptr<uint32_t>(p->dval2), (int)NV, 0, end_bit, s);
+    }));
+    launch_k1_fix_ties(ptr<uint64_t>(p->dkey2), ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
+                       s);
+    launch_k1_gather_counts(ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->ntiles),
+                            ptr<uint32_t>(p->cnt_sorted), NV, s);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceScan::ExclusiveSum(tmp, bytes, ptr<uint32_t>(p->cnt_sorted),
+                                           ptr<uint32_t>(p->off_sorted), (int)NV, s);
+    }));
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceScan::ExclusiveSum(tmp, bytes, ptr<uint32_t>(p->ntiles),
+                                           ptr<uint32_t>(p->inst_base), (int)NV, s);
+    }));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, ptr<uint32_t>(p->off_sorted) + (NV - 1), 4,
+                                cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 1, ptr<uint32_t>(p->cnt_sorted) + (NV - 1), 4,
+                                cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaStreamSynchronize(s));
+    p->n_inst = (int64_t)p->host_small[0] + (int64_t)p->host_small[1];
+  } else {
+    p->n_inst = 0;
+  }
+  p->mark_end(ST_DEPTH_SORT, e1, s);
+
+  cudaEvent_t e2 = p->mark_begin(s);
+  const int64_t ni = p->n_inst;
+  ENSURE(p->tkey, 4 * (ni + 1));
+  ENSURE(p->tkey2, 4 * (ni + 1));
+  ENSURE(p->tval, 4 * (ni + 1));
+  ENSURE(p->tval2, 4 * (ni + 1));
+  TS_CUDA_TRY(cudaMemsetAsync(p->range.p, 0, 8 * ntile_total, s));
+  if (ni > 0) {
+    launch_k1_emit(ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->cnt_sorted), ptr<uint32_t>(p->off_sorted),
+                   ptr<RasterRec>(p->rec), NV, n, p->tiles_x, p->tpv, ptr<uint32_t>(p->tkey),
+                   ptr<uint32_t>(p->tval), s);
+    const int tbits = bits_for((uint64_t)ntile_total);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint32_t>(p->tkey),
+                                             ptr<uint32_t>(p->tkey2), ptr<uint32_t>(p->tval),
+                                             ptr<uint32_t>(p->tval2), (int)ni, 0, tbits, s);
+    }));
+    launch_k1_tile_ranges(ptr<uint32_t>(p->tkey2), ni, ptr<uint32_t>(p->range), s);
+  }
+  TS_CUDA_TRY(cudaGetLastError());
+  p->mark_end(ST_TILE_SORT, e2, s);
+  return TS_OK;
+}
+
+ts_motions internal_motions(ts_plan *p) {
+  ts_motions m;
+  m.status = ptr<int8_t>(p->mot_status);
+  m.a = ptr<double>(p->mot_a);
+  m.b = ptr<double>(p->mot_b);
+  m.weight_sum = ptr<double>(p->mot_w);
+  m.pixel_count = ptr<int32_t>(p->mot_cnt);
+  m.static_pixel_count = ptr<int32_t>(p->mot_scnt);
+  m.static_weight_sum = ptr<double>(p->mot_sw);
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ts_version(void) { return 1; }
+
+const char *ts_error_string(int code) {
+  switch (code) {
+    case TS_OK: return "ok";
+    case TS_E_INVALID_ARGUMENT: return "invalid argument";
+    case TS_E_DIMENSION_MISMATCH: return "dimension mismatch";
+    case TS_E_CUDA: return "CUDA runtime error";
+    case TS_E_OUT_OF_MEMORY: return "out of device memory";
+    case TS_E_CAPACITY: return "capacity exceeded";
+    default: return "unknown error";
+  }
+}
+
+int ts_plan_create(ts_plan **plan) {
+  if (!plan) return TS_E_INVALID_ARGUMENT;
+  ts_plan *p = new (std::nothrow) ts_plan();
+  if (!p) return TS_E_OUT_OF_MEMORY;
+  p->cfg.alpha_cutoff = 1.0 / 255.0;
+  p->cfg.early_stop = 1e-4;
+  p->cfg.det_floor = 1e-12;
+  p->cfg.min_weight = 1e-3;
+  p->cfg.min_total_weight = 1e-3;
+  p->cfg.static_threshold_px = 1.0;
+  p->cfg.eig_floor = 1e-12;
+  p->cfg.min_pixels = 3;
+  p->cfg.min_views = 2;
+  p->cfg.min_total_pixels = 3;
+  *plan = p;
+  return TS_OK;
+}
+
+int ts_plan_destroy(ts_plan *p) {
+  if (!p) return TS_OK;
+  cudaDeviceSynchronize();
+  release_all(p);
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  if (p->host_small) cudaFreeHost(p->host_small);
+  delete p;
+  return TS_OK;
+}
+
+int64_t ts_plan_workspace_bytes(const ts_plan *p) { return p ? sum_workspace(p) : 0; }
+
+// Stage timing (CUDA events on the plan's launch stream), used by bench.py for the roofline.
+int ts_plan_timing(ts_plan *p, int enable) {
+  if (!p) return TS_E_INVALID_ARGUMENT;
+  p->timing = enable != 0;
+  p->ev_marks.clear();
+  p->ev_next = 0;
+  return TS_OK;
+}
+
+// Sums the recorded stage times (ms) into totals[ST_N] and counts[ST_N]; synchronises the events.
+int ts_plan_timing_read(ts_plan *p, double *totals_ms, int32_t *counts, int32_t n_stages) {
+  if (!p || !totals_ms || n_stages < ST_N) return TS_E_INVALID_ARGUMENT;
+  for (int i = 0; i < n_stages; i++) {
+    totals_ms[i] = 0.0;
+    if (counts) counts[i] = 0;
+  }
+  for (auto &m : p->ev_marks) {
+    TS_CUDA_TRY(cudaEventSynchronize(m.second.second));
+    float ms = 0.f;
+    TS_CUDA_TRY(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
+    totals_ms[m.first] += ms;
+    if (counts) counts[m.first]++;
+  }
+  return TS_OK;
+}
+
+int ts_project(const double *gaussians, int64_t n, const ts_camera *camera, double *mean2,
+               double *depth, double *cov2, uint8_t *in_front, void *stream) {
+  if (!camera || n < 0) return TS_E_INVALID_ARGUMENT;
+  launch_project_view(gaussians, n, *camera, mean2, depth, cov2, in_front, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_camera *cameras,
+                 int32_t n_views, const ts_config *config, void *stream) {
+  if (!plan) return TS_E_INVALID_ARGUMENT;
+  return frame_bin(plan, gaussians, n, cameras, n_views, config, (cudaStream_t)stream);
+}
+
+int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtype,
+                        const uint8_t *track_valid, const ts_motions *motions,
+                        const ts_updates *updates, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || !updates || p->V < 1) return TS_E_INVALID_ARGUMENT;
+  if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
+  const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
+  ENSURE(p->partial, sizeof(Partial) * (ni + 1));
+  ENSURE(p->flag, ni + 1);
+  ts_motions m = motions ? *motions : ts_motions{};
+  ts_motions im;
+  {
+    ENSURE(p->mot_status, NV + 1);
+    ENSURE(p->mot_a, 32 * (NV + 1));
+    ENSURE(p->mot_b, 16 * (NV + 1));
+    ENSURE(p->mot_w, 8 * (NV + 1));
+    ENSURE(p->mot_cnt, 4 * (NV + 1));
+    ENSURE(p->mot_scnt, 4 * (NV + 1));
+    ENSURE(p->mot_sw, 8 * (NV + 1));
+    im = internal_motions(p);
+  }
+  if (!m.status) m.status = im.status;
+  if (!m.a) m.a = im.a;
+  if (!m.b) m.b = im.b;
+  if (!m.weight_sum) m.weight_sum = im.weight_sum;
+  if (!m.pixel_count) m.pixel_count = im.pixel_count;
+
+  cudaEvent_t e3 = p->mark_begin(s);
+  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ni + 1, s));
+  TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
+                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), track_target,
+                        track_valid, n, p->W, p->H, p->tiles_x, p->tpv, p->tpv * p->V, 0, p->cfg,
+                        ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, s));
+  p->mark_end(ST_RASTER, e3, s);
+
+  cudaEvent_t e4 = p->mark_begin(s);
+  launch_k3_solve(ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), ptr<uint32_t>(p->inst_base),
+                  ptr<uint32_t>(p->ntiles), ptr<RasterRec>(p->rec), NV, p->cfg, m, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  p->mark_end(ST_SOLVE, e4, s);
+
+  cudaEvent_t e5 = p->mark_begin(s);
+  launch_k4_fuse(p->gaussians, n, ptr<ts_camera>(p->cams), p->V, m, p->cfg, *updates, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  p->mark_end(ST_FUSE, e5, s);
+  return TS_OK;
+}
+
+int ts_frame_binning(const ts_plan *p, ts_binning *out) {
+  if (!p || !out) return TS_E_INVALID_ARGUMENT;
+  out->n_instances = p->n_inst;
+  out->tiles_x = p->tiles_x;
+  out->tiles_y = p->tiles_y;
+  out->n_views = p->V;
+  out->inst_tile = p->tkey2.as<uint32_t>();
+  out->inst_gv = p->tval2.as<uint32_t>();
+  out->tile_range = p->range.as<uint32_t>();
+  out->gv_status = p->status.as<int8_t>();
+  out->gv_bbox = p->bbox.as<int16_t>();
+  return TS_OK;
+}
+
+int ts_rasterize_weights(ts_plan *p, const double *gaussians, int64_t n, const ts_camera *camera,
+                         double alpha_cutoff, double early_stop, int64_t *n_out,
+                         int64_t *n_degenerate_out, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || !camera || !n_out) return TS_E_INVALID_ARGUMENT;
+  if (!(alpha_cutoff > 0.0 && alpha_cutoff < 1.0)) return TS_E_INVALID_ARGUMENT;
+  ts_config cfg = p->cfg;
+  cfg.alpha_cutoff = alpha_cutoff;
+  cfg.early_stop = early_stop;
+  int rc = frame_bin(p, gaussians, n, camera, 1, &cfg, s);
+  if (rc) return rc;
+  // degenerate ids (splat.py:135-137), ascending
+  ENSURE(p->deg_flags, n + 1);
+  ENSURE(p->deg_ids, 8 * (n + 1));
+  ENSURE(p->deg_count, 8);
+  if (n > 0) {
+    k_degenerate_flags<<<nblk(n, 256), 256, 0, s>>>(ptr<int8_t>(p->status), n, ptr<uint8_t>(p->deg_flags));
+    cub::CountingInputIterator<int64_t> it(0);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceSelect::Flagged(tmp, bytes, it, ptr<uint8_t>(p->deg_flags),
+                                        ptr<int64_t>(p->deg_ids), ptr<int64_t>(p->deg_count), (int)n,
+                                        s);
+    }));
+  } else {
+    TS_CUDA_TRY(cudaMemsetAsync(p->deg_count.p, 0, 8, s));
+  }
+  int64_t cap = p->emit_key.bytes / 8;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    if (cap > 0) {
+      ENSURE(p->emit_key, 8 * cap);
+      ENSURE(p->emit_gv, 4 * cap);
+      ENSURE(p->emit_alpha, 8 * cap);
+      ENSURE(p->emit_trans, 8 * cap);
+    }
+    ENSURE(p->emit_count, 8);
+    TS_CUDA_TRY(cudaMemsetAsync(p->emit_count.p, 0, 8, s));
+    TS_CUDA_TRY(launch_k2(K2_EMIT, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
+                          ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), nullptr, nullptr, n,
+                          p->W, p->H, p->tiles_x, p->tpv, p->tpv, 0, cfg, nullptr, nullptr,
+                          ptr<unsigned long long>(p->emit_count), cap, ptr<uint64_t>(p->emit_key),
+                          ptr<uint32_t>(p->emit_gv), ptr<double>(p->emit_alpha),
+                          ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, s));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, p->emit_count.p, 8, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 2, p->deg_count.p, 8, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaStreamSynchronize(s));
+    uint64_t got = 0;
+    std::memcpy(&got, p->host_small, 8);
+    std::memcpy(&p->n_deg, p->host_small + 2, 8);
+    if ((int64_t)got <= cap) {
+      p->emit_n = (int64_t)got;
+      break;
+    }
+    cap = (int64_t)got;
+  }
+  const int64_t m = p->emit_n;
+  ENSURE(p->emit_key2, 8 * (m + 1));
+  ENSURE(p->emit_idx, 4 * (m + 1));
+  ENSURE(p->emit_idx2, 4 * (m + 1));
+  if (m > 0) {
+    k_iota<<<nblk(m, 256), 256, 0, s>>>(ptr<uint32_t>(p->emit_idx), m);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint64_t>(p->emit_key),
+                                             ptr<uint64_t>(p->emit_key2), ptr<uint32_t>(p->emit_idx),
+                                             ptr<uint32_t>(p->emit_idx2), (int)m, 0, 64, s);
+    }));
+  }
+  TS_CUDA_TRY(cudaGetLastError());
+  *n_out = m;
+  if (n_degenerate_out) *n_degenerate_out = p->n_deg;
+  return TS_OK;
+}
+
+int ts_rasterize_fetch(ts_plan *p, int32_t *pixel_x, int32_t *pixel_y, int64_t *gaussian_id,
+                       double *alpha, double *transmittance, double *depth,
+                       int64_t *degenerate_ids, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p) return TS_E_INVALID_ARGUMENT;
+  const int64_t m = p->emit_n;
+  if (m > 0)
+    k_fetch_contribs<<<nblk(m, 256), 256, 0, s>>>(
+        ptr<uint64_t>(p->emit_key2), ptr<uint32_t>(p->emit_idx2), ptr<uint32_t>(p->emit_gv),
+        ptr<double>(p->emit_alpha), ptr<double>(p->emit_trans), ptr<RasterRec>(p->rec),
+        ptr<double>(p->depth64), m, p->W, pixel_x, pixel_y, gaussian_id, alpha, transmittance,
+        depth);
+  if (p->n_deg > 0 && degenerate_ids)
+    TS_CUDA_TRY(cudaMemcpyAsync(degenerate_ids, p->deg_ids.p, 8 * p->n_deg,
+                                cudaMemcpyDeviceToDevice, s));
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_accumulate_view(ts_plan *p, const int32_t *pixel_x, const int32_t *pixel_y,
+                       const int64_t *gaussian_id, const double *alpha,
+                       const double *transmittance, int64_t m, int32_t width, int32_t height,
+                       const void *track_target, int32_t track_dtype, const uint8_t *track_valid,
+                       int64_t n, double static_threshold_px, double *v1, double *v2,
+                       double *weight_sum, int64_t *pixel_count, int64_t *static_pixel_count,
+                       double *static_weight_sum, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || m < 0 || n < 0 || width <= 0 || height <= 0) return TS_E_INVALID_ARGUMENT;
+  if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
+  if (n >= 0xFFFFFFFFll || m >= 0xFFFFFFFFll) return TS_E_INVALID_ARGUMENT;
+  ENSURE(p->seg_start, 4 * (n + 1));
+  ENSURE(p->seg_end, 4 * (n + 1));
+  ENSURE(p->acc_keys, 4 * (m + 1));
+  ENSURE(p->acc_keys2, 4 * (m + 1));
+  ENSURE(p->acc_iota, 4 * (m + 1));
+  ENSURE(p->acc_order, 4 * (m + 1));
+  TS_CUDA_TRY(cudaMemsetAsync(p->seg_start.p, 0, 4 * (n + 1), s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->seg_end.p, 0, 4 * (n + 1), s));
+  if (m > 0) {
+    k_gid_keys<<<nblk(m, 256), 256, 0, s>>>(gaussian_id, ptr<uint32_t>(p->acc_keys), m);
+    k_iota<<<nblk(m, 256), 256, 0, s>>>(ptr<uint32_t>(p->acc_iota), m);
+    const int kb = bits_for((uint64_t)n + 1);
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint32_t>(p->acc_keys),
+                                             ptr<uint32_t>(p->acc_keys2), ptr<uint32_t>(p->acc_iota),
+                                             ptr<uint32_t>(p->acc_order), (int)m, 0, kb, s);
+    }));
+    launch_segment_bounds(ptr<uint32_t>(p->acc_keys2), m, ptr<uint32_t>(p->seg_start),
+                          ptr<uint32_t>(p->seg_end), s);
+  }
+  launch_accumulate(n, ptr<uint32_t>(p->seg_start), ptr<uint32_t>(p->seg_end),
+                    ptr<uint32_t>(p->acc_order), pixel_x, pixel_y, alpha, transmittance, width,
+                    track_target, track_dtype, track_valid, static_threshold_px, v1, v2,
+                    weight_sum, pixel_count, static_pixel_count, static_weight_sum, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_solve_view(const double *v1, const double *v2, const double *weight_sum,
+                  const int64_t *pixel_count, int64_t n, double det_floor, int32_t min_pixels,
+                  double min_weight, int8_t *status, double *a, double *b, double *det,
+                  void *stream) {
+  if (n < 0) return TS_E_INVALID_ARGUMENT;
+  launch_solve_abs(v1, v2, weight_sum, pixel_count, n, det_floor, min_pixels, min_weight, status,
+                   a, b, det, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_update_all(const double *gaussians, int64_t n, const ts_camera *cameras, int32_t n_views,
+                  const ts_motions *motions, const ts_config *config, const ts_updates *updates,
+                  void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!cameras || n_views < 1 || !motions || !config || !updates || n < 0)
+    return TS_E_INVALID_ARGUMENT;
+  void *dcams = nullptr;
+  TS_CUDA_TRY(cudaMallocAsync(&dcams, sizeof(ts_camera) * n_views, s));
+  TS_CUDA_TRY(cudaMemcpyAsync(dcams, cameras, sizeof(ts_camera) * n_views, cudaMemcpyHostToDevice, s));
+  launch_k4_fuse(gaussians, n, reinterpret_cast<ts_camera *>(dcams), n_views, *motions, *config,
+                 *updates, s);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dcams, s);
+  return e == cudaSuccess ? TS_OK : TS_E_CUDA;
+}
+
+int ts_debug_fuse_one(const double *gaussians, int64_t n, const ts_camera *cameras,
+                      int32_t n_views, const ts_motions *motions, const ts_config *config,
+                      int64_t g, double *dbg, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  void *dcams = nullptr;
+  TS_CUDA_TRY(cudaMallocAsync(&dcams, sizeof(ts_camera) * n_views, s));
+  TS_CUDA_TRY(cudaMemcpyAsync(dcams, cameras, sizeof(ts_camera) * n_views, cudaMemcpyHostToDevice, s));
+  launch_k4_debug(gaussians, n, reinterpret_cast<ts_camera *>(dcams), n_views, *motions, *config, g,
+                  dbg, s);
+  cudaFreeAsync(dcams, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch, int32_t max_rows,
+                         double *x, int8_t *status, void *stream) {
+  launch_triangulate_batch(rows, n_rows, batch, max_rows, x, status, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_solve_cov3d_batch(const double *lin, const double *rhs, const int32_t *n_rows,
+                         int64_t batch, int32_t max_rows, double *x, int8_t *status,
+                         void *stream) {
+  launch_cov3d_batch(lin, rhs, n_rows, batch, max_rows, x, status, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_decompose_batch(const double *sigma, const double *ref_quat, int64_t batch,
+                       double eig_floor, double *quat, double *scale, int8_t *status,
+                       void *stream) {
+  launch_decompose_batch(sigma, ref_quat, batch, eig_floor, quat, scale, status,
+                         (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_dominant_gaussians(ts_plan *p, int32_t view, int64_t *gid_img, double *depth_img,
+                          void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || view < 0 || view >= p->V) return TS_E_INVALID_ARGUMENT;
+  // pixels no tile touches stay at -1 / 0
+  TS_CUDA_TRY(cudaMemsetAsync(gid_img, 0xFF, 8 * (size_t)p->W * p->H, s));
+  TS_CUDA_TRY(cudaMemsetAsync(depth_img, 0, 8 * (size_t)p->W * p->H, s));
+  TS_CUDA_TRY(launch_k2(K2_DOMINANT, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
+                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), nullptr, nullptr,
+                        p->n, p->W, p->H, p->tiles_x, p->tpv, p->tpv, view * p->tpv, p->cfg,
+                        nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
+                        ptr<double>(p->depth64), gid_img, depth_img, s));
+  return TS_OK;
+}
+
+}  // extern "C"
+
+extern "C" int ts_memcpy_d2h(void *host_dst, const void *device_src, int64_t bytes) {
+  if (bytes < 0) return TS_E_INVALID_ARGUMENT;
+  if (bytes == 0) return TS_OK;
+  TS_CUDA_TRY(cudaMemcpy(host_dst, device_src, (size_t)bytes, cudaMemcpyDeviceToHost));
+  return TS_OK;
+}

@@ -1,0 +1,185 @@
+// binning.cu -- K1: projection + exact depth order + 16x16 tile binning (sm_100a).
+//
+// Reference: gausstrack/splat.py:80-110 (_project_all), :131-146 (footprint), :171-180 (order).
+// The reference has no tiles; a pixel's contributions are ordered by (depth, gid).  We order each
+// tile's Gaussian list by the same key, so every pixel of the tile sees its Gaussians in exactly
+// the reference order:
+//   1. k1_project: one thread per Gaussian, looping over the V cameras (the 88-byte Gaussian is
+//      read once): writes the 64-byte RasterRec, a 64-bit sort key (view << 32 | f32(depth) bits)
+//      and the tile count of its bbox.
+//   2. CUB radix sort by that key (37 bits at V=20).  f32 rounding is monotone, so the order is
+//      right except inside runs of equal f32 depth; k1_fix_ties re-sorts those (short) runs by
+//      the exact (f64 depth, gid) key.
+//   3. k1_emit writes one (tile, gv) instance per covered tile in that depth order; a stable CUB
+//      radix sort on the tile id alone then yields tile-major, depth-ordered lists.
+//   4. k1_tile_ranges marks [start, end) of every tile.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ts {
+
+__global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, int64_t n,
+                                                  const ts_camera *__restrict__ cams, int V,
+                                                  RasterRec *__restrict__ rec,
+                                                  uint64_t *__restrict__ dkey,
+                                                  uint32_t *__restrict__ dval,
+                                                  double *__restrict__ depth64,
+                                                  uint32_t *__restrict__ ntiles,
+                                                  int8_t *__restrict__ status,
+                                                  int16_t *__restrict__ bbox) {
+  extern __shared__ ts_camera s_cam[];
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam[i] = cams[i];
+  __syncthreads();
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double gs[11];
+#pragma unroll
+  for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
+  double c3[9];
+  covariance3d(gs, c3);
+  for (int v = 0; v < V; v++) {
+    const ts_camera &cam = s_cam[v];
+    Projection p;
+    project(gs, c3, cam, p);
+    RasterRec r;
+    int st = footprint(p, gs[10], cam.width, cam.height, r);
+    int64_t gv = (int64_t)v * n + g;
+    status[gv] = (int8_t)st;
+    uint64_t key = ((uint64_t)v << 32);
+    uint32_t nt = 0;
+    int16_t bb[4] = {0, -1, 0, -1};
+    if (st == 3) {
+      r.g = (uint32_t)g;
+      r.pad = 0;
+      rec[gv] = r;
+      key |= (uint64_t)__float_as_uint(__double2float_rn(p.depth));
+      nt = (uint32_t)((r.x1 / TS_TILE - r.x0 / TS_TILE + 1) * (r.y1 / TS_TILE - r.y0 / TS_TILE + 1));
+      bb[0] = r.x0; bb[1] = r.x1; bb[2] = r.y0; bb[3] = r.y1;
+    } else {
+      key |= 0xFFFFFFFFull;  // sorts after every binned Gaussian of the view, never emitted
+    }
+    dkey[gv] = key;
+    dval[gv] = (uint32_t)gv;
+    depth64[gv] = p.depth;
+    ntiles[gv] = nt;
+    reinterpret_cast<short4 *>(bbox)[gv] = make_short4(bb[0], bb[1], bb[2], bb[3]);
+  }
+}
+
+// Re-sort runs of equal (view, f32 depth) keys by the exact (f64 depth, gid) key.
+__global__ void k1_fix_ties(const uint64_t *__restrict__ key, uint32_t *__restrict__ val,
+                            const double *__restrict__ depth64, int64_t M) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  uint64_t kk = key[k];
+  if ((uint32_t)kk == 0xFFFFFFFFu) return;
+  if (k > 0 && key[k - 1] == kk) return;
+  if (k + 1 >= M || key[k + 1] != kk) return;
+  int64_t e = k + 1;
+  while (e < M && key[e] == kk) e++;
+  for (int64_t i = k + 1; i < e; i++) {
+    uint32_t x = val[i];
+    double dx = depth64[x];
+    int64_t j = i - 1;
+    while (j >= k) {
+      uint32_t y = val[j];
+      double dy = depth64[y];
+      if (dy < dx || (dy == dx && y < x)) break;
+      val[j + 1] = y;
+      j--;
+    }
+    val[j + 1] = x;
+  }
+}
+
+__global__ void k1_gather_counts(const uint32_t *__restrict__ val, const uint32_t *__restrict__ ntiles,
+                                 uint32_t *__restrict__ cnt_sorted, int64_t M) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < M) cnt_sorted[k] = ntiles[val[k]];
+}
+
+__global__ void k1_emit(const uint32_t *__restrict__ val, const uint32_t *__restrict__ cnt_sorted,
+                        const uint32_t *__restrict__ off_sorted, const RasterRec *__restrict__ rec,
+                        int64_t M, int64_t n, int tiles_x, int tiles_per_view,
+                        uint32_t *__restrict__ tkey, uint32_t *__restrict__ tval) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  uint32_t c = cnt_sorted[k];
+  if (c == 0) return;
+  uint32_t gv = val[k];
+  uint32_t v = (uint32_t)(gv / n);
+  RasterRec r = rec[gv];
+  uint32_t o = off_sorted[k];
+  uint32_t base = v * (uint32_t)tiles_per_view;
+  for (int ty = r.y0 / TS_TILE; ty <= r.y1 / TS_TILE; ty++)
+    for (int tx = r.x0 / TS_TILE; tx <= r.x1 / TS_TILE; tx++) {
+      tkey[o] = base + (uint32_t)(ty * tiles_x + tx);
+      tval[o] = gv;
+      o++;
+    }
+}
+
+__global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, int64_t n_inst,
+                               uint32_t *__restrict__ range) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_inst) return;
+  uint32_t t = tkey[i];
+  if (i == 0 || tkey[i - 1] != t) range[2 * t] = (uint32_t)i;
+  if (i == n_inst - 1 || tkey[i + 1] != t) range[2 * t + 1] = (uint32_t)(i + 1);
+}
+
+// _project_all for the stage API (one view).
+__global__ void k_project_view(const double *__restrict__ G, int64_t n, ts_camera cam,
+                               double *__restrict__ mean2, double *__restrict__ depth,
+                               double *__restrict__ cov2, uint8_t *__restrict__ in_front) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double gs[11];
+#pragma unroll
+  for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
+  double c3[9];
+  covariance3d(gs, c3);
+  Projection p;
+  project(gs, c3, cam, p);
+  mean2[2 * g] = p.mean2[0];
+  mean2[2 * g + 1] = p.mean2[1];
+  depth[g] = p.depth;
+  cov2[3 * g] = p.cov2[0];
+  cov2[3 * g + 1] = p.cov2[1];
+  cov2[3 * g + 2] = p.cov2[2];
+  in_front[g] = p.in_front;
+}
+
+static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
+                       uint64_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
+                       int8_t *status, int16_t *bbox, cudaStream_t s) {
+  if (n == 0) return;
+  k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, dkey, dval,
+                                                                  depth64, ntiles, status, bbox);
+}
+void launch_k1_fix_ties(const uint64_t *key, uint32_t *val, const double *depth64, int64_t M,
+                        cudaStream_t s) {
+  if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M);
+}
+void launch_k1_gather_counts(const uint32_t *val, const uint32_t *ntiles, uint32_t *cnt_sorted,
+                             int64_t M, cudaStream_t s) {
+  if (M) k1_gather_counts<<<blocks(M, 256), 256, 0, s>>>(val, ntiles, cnt_sorted, M);
+}
+void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint32_t *off_sorted,
+                    const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
+                    uint32_t *tkey, uint32_t *tval, cudaStream_t s) {
+  if (M)
+    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, cnt_sorted, off_sorted, rec, M, n, tiles_x,
+                                           tiles_per_view, tkey, tval);
+}
+void launch_k1_tile_ranges(const uint32_t *tkey, int64_t n_inst, uint32_t *range, cudaStream_t s) {
+  if (n_inst) k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, n_inst, range);
+}
+void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
+                         double *depth, double *cov2, uint8_t *in_front, cudaStream_t s) {
+  if (n) k_project_view<<<blocks(n, 128), 128, 0, s>>>(G, n, cam, mean2, depth, cov2, in_front);
+}
+
+}  // namespace ts

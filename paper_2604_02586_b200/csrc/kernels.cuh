@@ -1,0 +1,64 @@
+// kernels.cuh -- internal launcher declarations shared by the .cu files of the library.
+#pragma once
+
+#include "common.cuh"
+
+namespace ts {
+
+enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
+
+void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
+                       uint64_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
+                       int8_t *status, int16_t *bbox, cudaStream_t s);
+void launch_k1_fix_ties(const uint64_t *key, uint32_t *val, const double *depth64, int64_t M,
+                        cudaStream_t s);
+void launch_k1_gather_counts(const uint32_t *val, const uint32_t *ntiles, uint32_t *cnt_sorted,
+                             int64_t M, cudaStream_t s);
+void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint32_t *off_sorted,
+                    const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
+                    uint32_t *tkey, uint32_t *tval, cudaStream_t s);
+void launch_k1_tile_ranges(const uint32_t *tkey, int64_t n_inst, uint32_t *range, cudaStream_t s);
+void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
+                         double *depth, double *cov2, uint8_t *in_front, cudaStream_t s);
+
+cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uint32_t *inst_gv,
+                      const uint32_t *tile_range, const uint32_t *inst_base,
+                      const void *track_target, const uint8_t *track_valid, int64_t n, int W,
+                      int H, int tiles_x, int tiles_per_view, int n_tiles_total,
+                      int tile_offset, const ts_config &cfg, Partial *partial, uint8_t *flag,
+                      unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
+                      uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
+                      const double *depth64, int64_t *dom_gid, double *dom_depth,
+                      cudaStream_t s);
+
+// K3: per-(view, Gaussian) affine fit from the tile partials of K2.
+void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
+                     const uint32_t *ntiles, const RasterRec *rec, int64_t nv_total,
+                     const ts_config &cfg, ts_motions m, cudaStream_t s);
+// solve_view on absolute moments (stage API)
+void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
+                      int64_t n, double det_floor, int min_pixels, double min_weight,
+                      int8_t *status, double *a, double *b, double *det, cudaStream_t s);
+// accumulate_view over explicit contributions, stably sorted by gid: one thread per Gaussian
+void launch_segment_bounds(const uint32_t *sorted_gid, int64_t m, uint32_t *seg_start,
+                           uint32_t *seg_end, cudaStream_t s);
+void launch_accumulate(int64_t n, const uint32_t *seg_start, const uint32_t *seg_end,
+                       const uint32_t *order, const int32_t *px, const int32_t *py,
+                       const double *alpha, const double *trans, int W, const void *target,
+                       int track_dtype, const uint8_t *valid, double thr, double *v1, double *v2,
+                       double *wsum, int64_t *cnt, int64_t *scnt, double *swsum, cudaStream_t s);
+
+// K4: multi-view fuse (update_all)
+void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
+                    const ts_config &cfg, ts_updates u, cudaStream_t s);
+void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
+                     const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s);
+void launch_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch,
+                              int max_rows, double *x, int8_t *status, cudaStream_t s);
+void launch_cov3d_batch(const double *lin, const double *rhs, const int32_t *n_rows,
+                        int64_t batch, int max_rows, double *x, int8_t *status, cudaStream_t s);
+void launch_decompose_batch(const double *sigma, const double *ref_quat, int64_t batch,
+                            double eig_floor, double *quat, double *scale, int8_t *status,
+                            cudaStream_t s);
+
+}  // namespace ts

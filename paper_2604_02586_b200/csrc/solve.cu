@@ -1,0 +1,271 @@
+// solve.cu -- K3 per-(view, Gaussian) affine fit + the accumulate_view stage kernel (sm_100a).
+//
+// K3 (fused path): one thread per (view, Gaussian).  It sums the Gaussian's tile partials written
+// by K2 in fixed instance order (deterministic), builds the anchored moment matrices
+//     V1a = sum w h h^T,  V2a = sum w h x'_a^T,   h = [x - a; 1], x'_a = x' - a
+// (a = integer anchor of the view bbox), applies the solve_view eligibility rule
+// (motion2d.py:168-170: count >= min_pixels, sum w >= min_weight, det(V1) >= det_floor; det is
+// translation invariant so it is taken on V1a), solves V1a [A^T; b_a^T] = V2a with partial-pivot LU
+// (motion2d.py:173, LAPACK gesv) and maps back: b = b_a + a - A a.  Anchoring keeps V1 at
+// cond ~1e2 instead of the 1e10-1e14 of absolute pixel moments.
+//
+// Stage accumulate_view (motion2d.py:126-161): contributions are stably sorted by Gaussian id and
+// one thread per Gaussian adds them in array order with the reference's exact products
+// ((w*h_i)*h_j, no FMA), so the result equals np.add.at bit-for-bit.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ts {
+
+// Partial-pivot LU solve of a 3x3 system with 2 right-hand sides.  Returns det(A).
+__device__ __forceinline__ double lu3_solve(double A[3][3], double B[3][2]) {
+  double det = 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    int piv = k;
+    double best = fabs(A[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < 3; i++)
+      if (fabs(A[i][k]) > best) {
+        best = fabs(A[i][k]);
+        piv = i;
+      }
+    if (piv != k) {
+      det = -det;
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        double t = A[k][j];
+        A[k][j] = A[piv][j];
+        A[piv][j] = t;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        double t = B[k][j];
+        B[k][j] = B[piv][j];
+        B[piv][j] = t;
+      }
+    }
+    const double d = A[k][k];
+    det *= d;
+    if (d == 0.0) continue;
+#pragma unroll
+    for (int i = k + 1; i < 3; i++) {
+      const double l = A[i][k] / d;
+#pragma unroll
+      for (int j = k + 1; j < 3; j++) A[i][j] -= l * A[k][j];
+#pragma unroll
+      for (int j = 0; j < 2; j++) B[i][j] -= l * B[k][j];
+    }
+  }
+  if (det != 0.0) {
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+#pragma unroll
+      for (int i = 2; i >= 0; i--) {
+        double s = B[i][j];
+#pragma unroll
+        for (int k = i + 1; k < 3; k++) s -= A[i][k] * B[k][j];
+        B[i][j] = s / A[i][i];
+      }
+    }
+  }
+  return det;
+}
+
+__device__ __forceinline__ bool finite6(const double *x) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 6; i++) ok = ok && isfinite(x[i]);
+  return ok;
+}
+
+__global__ void __launch_bounds__(256) k3_solve(const Partial *__restrict__ partial,
+                                                const uint8_t *__restrict__ flag,
+                                                const uint32_t *__restrict__ inst_base,
+                                                const uint32_t *__restrict__ ntiles,
+                                                const RasterRec *__restrict__ rec,
+                                                int64_t NV, double det_floor, int min_pixels,
+                                                double min_weight, ts_motions m) {
+  int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gv >= NV) return;
+  const uint32_t nt = ntiles[gv];
+  double mom[TS_NMOM];
+#pragma unroll
+  for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
+  uint32_t cnt = 0, scnt = 0;
+  double ax = 0.0, ay = 0.0;
+  if (nt) {
+    const uint32_t base = inst_base[gv];
+    for (uint32_t i = 0; i < nt; i++) {
+      if (!flag[base + i]) continue;
+      const Partial &p = partial[base + i];
+#pragma unroll
+      for (int k = 0; k < TS_NMOM; k++) mom[k] += p.m[k];
+      cnt += p.count;
+      scnt += p.static_count;
+    }
+    const RasterRec r = rec[gv];
+    ax = (double)anchor_x(r);
+    ay = (double)anchor_y(r);
+  }
+  int8_t status = TS_STATUS_UNSOLVABLE;
+  double A[4] = {1.0, 0.0, 0.0, 1.0}, bvec[2] = {0.0, 0.0};
+  if ((int)cnt >= min_pixels && mom[0] >= min_weight) {
+    double V1[3][3] = {{mom[3], mom[4], mom[1]}, {mom[4], mom[5], mom[2]}, {mom[1], mom[2], mom[0]}};
+    double X[3][2] = {{mom[8], mom[9]}, {mom[10], mom[11]}, {mom[6], mom[7]}};
+    const double det = lu3_solve(V1, X);
+    if (det >= det_floor) {
+      // ab = [A^T; b_a^T] -> A = ab[:2].T, b_a = ab[2]  (motion2d.py:177)
+      double a00 = X[0][0], a01 = X[1][0], a10 = X[0][1], a11 = X[1][1];
+      double b0 = X[2][0] + ax - (a00 * ax + a01 * ay);
+      double b1 = X[2][1] + ay - (a10 * ax + a11 * ay);
+      double res[6] = {a00, a01, a10, a11, b0, b1};
+      if (finite6(res)) {
+        status = TS_STATUS_SOLVED;
+        A[0] = a00; A[1] = a01; A[2] = a10; A[3] = a11;
+        bvec[0] = b0; bvec[1] = b1;
+      }
+    }
+  }
+  m.status[gv] = status;
+  reinterpret_cast<double2 *>(m.a)[2 * gv] = make_double2(A[0], A[1]);
+  reinterpret_cast<double2 *>(m.a)[2 * gv + 1] = make_double2(A[2], A[3]);
+  reinterpret_cast<double2 *>(m.b)[gv] = make_double2(bvec[0], bvec[1]);
+  m.weight_sum[gv] = mom[0];
+  m.pixel_count[gv] = (int32_t)cnt;
+  if (m.static_pixel_count) m.static_pixel_count[gv] = (int32_t)scnt;
+  if (m.static_weight_sum) m.static_weight_sum[gv] = mom[12];
+}
+
+// solve_view on absolute moments (motion2d.py:164-184).
+__global__ void k_solve_abs(const double *__restrict__ v1, const double *__restrict__ v2,
+                            const double *__restrict__ wsum, const int64_t *__restrict__ cnt,
+                            int64_t n, double det_floor, int min_pixels, double min_weight,
+                            int8_t *status, double *a, double *b, double *det_out) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double V1[3][3], X[3][2];
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+#pragma unroll
+    for (int j = 0; j < 3; j++) V1[i][j] = v1[9 * g + 3 * i + j];
+#pragma unroll
+    for (int j = 0; j < 2; j++) X[i][j] = v2[6 * g + 2 * i + j];
+  }
+  const double det = lu3_solve(V1, X);
+  if (det_out) det_out[g] = det;
+  bool ok = cnt[g] >= min_pixels && wsum[g] >= min_weight && det >= det_floor;
+  double res[6] = {X[0][0], X[1][0], X[0][1], X[1][1], X[2][0], X[2][1]};
+  ok = ok && finite6(res);
+  status[g] = ok ? TS_STATUS_SOLVED : TS_STATUS_UNSOLVABLE;
+  a[4 * g] = ok ? res[0] : 1.0;
+  a[4 * g + 1] = ok ? res[1] : 0.0;
+  a[4 * g + 2] = ok ? res[2] : 0.0;
+  a[4 * g + 3] = ok ? res[3] : 1.0;
+  b[2 * g] = ok ? res[4] : 0.0;
+  b[2 * g + 1] = ok ? res[5] : 0.0;
+}
+
+__global__ void k_segment_bounds(const uint32_t *__restrict__ sorted_gid, int64_t m,
+                                 uint32_t *__restrict__ seg_start, uint32_t *__restrict__ seg_end) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  uint32_t g = sorted_gid[i];
+  if (i == 0 || sorted_gid[i - 1] != g) seg_start[g] = (uint32_t)i;
+  if (i == m - 1 || sorted_gid[i + 1] != g) seg_end[g] = (uint32_t)(i + 1);
+}
+
+template <typename TrackT>
+__global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ seg_start,
+                                      const uint32_t *__restrict__ seg_end,
+                                      const uint32_t *__restrict__ order,
+                                      const int32_t *__restrict__ px, const int32_t *__restrict__ py,
+                                      const double *__restrict__ alpha,
+                                      const double *__restrict__ trans, int W,
+                                      const TrackT *__restrict__ target,
+                                      const uint8_t *__restrict__ valid, double thr, double *v1,
+                                      double *v2, double *wsum, int64_t *cnt, int64_t *scnt,
+                                      double *swsum) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double s1[9], s2[6], sw = 0.0, ssw = 0.0;
+  int64_t c = 0, sc = 0;
+#pragma unroll
+  for (int k = 0; k < 9; k++) s1[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; k++) s2[k] = 0.0;
+  const uint32_t s = seg_start[g], e = seg_end[g];
+  for (uint32_t i = s; i < e; i++) {
+    const uint32_t k = order[i];
+    const int x = px[k], y = py[k];
+    const int64_t pix = (int64_t)y * W + x;
+    if (!valid[pix]) continue;
+    const double xp0 = (double)target[2 * pix], xp1 = (double)target[2 * pix + 1];
+    const double w = mul(alpha[k], trans[k]);
+    const double h[3] = {(double)x, (double)y, 1.0};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const double wh = mul(w, h[a]);
+#pragma unroll
+      for (int b = 0; b < 3; b++) s1[3 * a + b] = add(s1[3 * a + b], mul(wh, h[b]));
+      s2[2 * a] = add(s2[2 * a], mul(wh, xp0));
+      s2[2 * a + 1] = add(s2[2 * a + 1], mul(wh, xp1));
+    }
+    sw = add(sw, w);
+    c++;
+    if (is_static(xp0, xp1, x, y, thr)) {
+      sc++;
+      ssw = add(ssw, w);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 9; k++) v1[9 * g + k] = s1[k];
+#pragma unroll
+  for (int k = 0; k < 6; k++) v2[6 * g + k] = s2[k];
+  wsum[g] = sw;
+  cnt[g] = c;
+  scnt[g] = sc;
+  swsum[g] = ssw;
+}
+
+static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
+                     const uint32_t *ntiles, const RasterRec *rec, int64_t nv_total,
+                     const ts_config &cfg, ts_motions m, cudaStream_t s) {
+  if (nv_total)
+    k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, rec, nv_total,
+                                                   cfg.det_floor, cfg.min_pixels, cfg.min_weight,
+                                                   m);
+}
+
+void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
+                      int64_t n, double det_floor, int min_pixels, double min_weight,
+                      int8_t *status, double *a, double *b, double *det, cudaStream_t s) {
+  if (n)
+    k_solve_abs<<<blocks(n, 256), 256, 0, s>>>(v1, v2, wsum, cnt, n, det_floor, min_pixels,
+                                               min_weight, status, a, b, det);
+}
+
+void launch_segment_bounds(const uint32_t *sorted_gid, int64_t m, uint32_t *seg_start,
+                           uint32_t *seg_end, cudaStream_t s) {
+  if (m) k_segment_bounds<<<blocks(m, 256), 256, 0, s>>>(sorted_gid, m, seg_start, seg_end);
+}
+
+void launch_accumulate(int64_t n, const uint32_t *seg_start, const uint32_t *seg_end,
+                       const uint32_t *order, const int32_t *px, const int32_t *py,
+                       const double *alpha, const double *trans, int W, const void *target,
+                       int track_dtype, const uint8_t *valid, double thr, double *v1, double *v2,
+                       double *wsum, int64_t *cnt, int64_t *scnt, double *swsum, cudaStream_t s) {
+  if (!n) return;
+  if (track_dtype == TS_TRACK_F32)
+    k_accumulate_segments<float><<<blocks(n, 128), 128, 0, s>>>(
+        n, seg_start, seg_end, order, px, py, alpha, trans, W,
+        reinterpret_cast<const float *>(target), valid, thr, v1, v2, wsum, cnt, scnt, swsum);
+  else
+    k_accumulate_segments<double><<<blocks(n, 128), 128, 0, s>>>(
+        n, seg_start, seg_end, order, px, py, alpha, trans, W,
+        reinterpret_cast<const double *>(target), valid, thr, v1, v2, wsum, cnt, scnt, swsum);
+}
+
+}  // namespace ts

@@ -1,0 +1,176 @@
+"""Batched, tensor-native engine of the hot path (the fused K1 -> K2 -> K3 -> K4 pipeline).
+
+This is the fast path under `compensate_frame`: Gaussians, cameras and tracks stay on the device
+as SoA tensors; reference-typed objects are only produced on demand by the API shims.
+
+    eng = FrameEngine()
+    eng.bin(gaussians, cameras, config)          # K1: once per clip (pipeline.py:191-196)
+    out = eng.compensate(track_target, valid)    # K2 + K3 + K4: once per target frame
+
+Layouts (device):
+    gaussians     (N, 11) float64    mean, quaternion (w,x,y,z), scale, opacity
+    track_target  (V, H, W, 2)       float32 (TRKF, fileio.py:108-136) or float64
+    track_valid   (V, H, W)          uint8
+    motions       SoA over gv = v*N + g: status int8, a (.,2,2) f64, b (.,2) f64,
+                  weight_sum f64, pixel_count i32, static_pixel_count i32, static_weight_sum f64
+    updates       delta_mean (N,3), rotation (N,4), scale (N,3) f64, status int8
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .core import cameras_array, gaussians_array
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def as_device(x, dtype, device=None):
+    """Host array / tensor -> contiguous CUDA tensor of `dtype` (no copy if already there)."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x))
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if t.device != dev or t.dtype != dtype:
+        t = t.to(device=dev, dtype=dtype, non_blocking=False)
+    return t.contiguous()
+
+
+@dataclass
+class FrameOutputs:
+    delta_mean: "object"
+    rotation: "object"
+    scale: "object"
+    status: "object"
+    motion_status: "object"
+    motion_a: "object"
+    motion_b: "object"
+    weight_sum: "object"
+    pixel_count: "object"
+    static_pixel_count: "object"
+    static_weight_sum: "object"
+
+    def tallies(self):
+        st = self.status
+        return {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
+                "unsolvable": int((st == 0).sum())}
+
+
+class FrameEngine:
+    """Holds the per-clip binning and per-frame workspace of one device."""
+
+    def __init__(self, plan: nat.Plan | None = None):
+        self.plan = plan if plan is not None else nat.Plan()
+        self._lib = nat.lib()
+        self.n = 0
+        self.n_views = 0
+        self.width = self.height = 0
+        self._gauss = None
+        self._cams = None
+
+    # -- K1 ------------------------------------------------------------------------------
+    def bin(self, gaussians, cameras, config=None, stream=None):
+        """Project + depth-order + tile-bin the first-frame Gaussians into every view."""
+        torch = _torch()
+        g = gaussians if isinstance(gaussians, torch.Tensor) else gaussians_array(gaussians)
+        self._gauss = as_device(g, torch.float64).reshape(-1, 11)
+        cam_rows = cameras_array(cameras)
+        self._cams = nat.make_cameras(cam_rows)
+        self._cfg = nat.make_config(config)
+        self.n = int(self._gauss.shape[0])
+        self.n_views = len(cam_rows)
+        self.width, self.height = int(cam_rows[0][16]), int(cam_rows[0][17])
+        nat.check(self._lib.ts_frame_bin(self.plan.handle, nat.dptr(self._gauss), self.n,
+                                         self._cams, self.n_views, ctypes.byref(self._cfg),
+                                         nat.stream_ptr(stream)), "ts_frame_bin")
+        return self
+
+    def binning(self):
+        """Copies of the binning arrays (tile keys, instance order, ranges, bbox, status)."""
+        torch = _torch()
+        b = nat.Binning()
+        nat.check(self._lib.ts_frame_binning(self.plan.handle, ctypes.byref(b)), "binning")
+        torch.cuda.synchronize()
+        ni = int(b.n_instances)
+        nt = int(b.tiles_x) * int(b.tiles_y) * int(b.n_views)
+        nv = self.n * self.n_views
+
+        def grab(ptr, count, dtype, width=1):
+            out = np.empty(count * width, dtype)
+            if count:
+                nat.check(self._lib.ts_memcpy_d2h(out.ctypes.data, ptr, out.nbytes), "d2h")
+            return out.reshape(count, width) if width > 1 else out
+
+        return dict(n_instances=ni, tiles_x=int(b.tiles_x), tiles_y=int(b.tiles_y),
+                    inst_tile=grab(b.inst_tile, ni, np.uint32),
+                    inst_gv=grab(b.inst_gv, ni, np.uint32),
+                    tile_range=grab(b.tile_range, nt, np.uint32, 2),
+                    status=grab(b.gv_status, nv, np.int8),
+                    bbox=grab(b.gv_bbox, nv, np.int16, 4))
+
+    # -- K2 + K3 + K4 ----------------------------------------------------------------------
+    def alloc_outputs(self):
+        torch = _torch()
+        n, nv = self.n, self.n * self.n_views
+        dev = self._gauss.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        return FrameOutputs(
+            delta_mean=torch.empty((n, 3), **f64), rotation=torch.empty((n, 4), **f64),
+            scale=torch.empty((n, 3), **f64), status=torch.empty(n, dtype=torch.int8, device=dev),
+            motion_status=torch.empty(nv, dtype=torch.int8, device=dev),
+            motion_a=torch.empty((nv, 2, 2), **f64), motion_b=torch.empty((nv, 2), **f64),
+            weight_sum=torch.empty(nv, **f64),
+            pixel_count=torch.empty(nv, dtype=torch.int32, device=dev),
+            static_pixel_count=torch.empty(nv, dtype=torch.int32, device=dev),
+            static_weight_sum=torch.empty(nv, **f64))
+
+    def compensate(self, track_target, track_valid, out: FrameOutputs | None = None,
+                   stream=None) -> FrameOutputs:
+        """Fused raster-accumulate, per-view affine fit and multi-view fuse for one frame."""
+        torch = _torch()
+        if self._gauss is None:
+            raise RuntimeError("FrameEngine.bin() must run before compensate()")
+        tgt = track_target
+        if not isinstance(tgt, torch.Tensor):
+            tgt = np.asarray(tgt)
+            tgt = as_device(tgt, torch.float32 if tgt.dtype == np.float32 else torch.float64)
+        else:
+            tgt = tgt.contiguous()
+        val = as_device(track_valid, torch.uint8)
+        expect = (self.n_views, self.height, self.width)
+        if tuple(tgt.shape) != expect + (2,) or tuple(val.shape) != expect:
+            from .errors import DimensionMismatch
+            raise DimensionMismatch(f"tracks {tuple(tgt.shape)} / {tuple(val.shape)} do not "
+                                    f"match {expect}")
+        dtype = nat.TS_TRACK_F32 if tgt.dtype == torch.float32 else nat.TS_TRACK_F64
+        if out is None:
+            out = self.alloc_outputs()
+        m = nat.Motions(nat.dptr(out.motion_status).value, nat.dptr(out.motion_a).value,
+                        nat.dptr(out.motion_b).value, nat.dptr(out.weight_sum).value,
+                        nat.dptr(out.pixel_count).value, nat.dptr(out.static_pixel_count).value,
+                        nat.dptr(out.static_weight_sum).value)
+        u = nat.Updates(nat.dptr(out.delta_mean).value, nat.dptr(out.rotation).value,
+                        nat.dptr(out.scale).value, nat.dptr(out.status).value)
+        nat.check(self._lib.ts_frame_compensate(self.plan.handle, nat.dptr(tgt), dtype,
+                                                nat.dptr(val), ctypes.byref(m), ctypes.byref(u),
+                                                nat.stream_ptr(stream)), "ts_frame_compensate")
+        return out
+
+    def dominant_gaussians(self, view, stream=None):
+        """Per-pixel dominant Gaussian id (-1 if none) and its depth (scene.py:166-189)."""
+        torch = _torch()
+        gid = torch.empty((self.height, self.width), dtype=torch.int64, device="cuda")
+        dep = torch.empty((self.height, self.width), dtype=torch.float64, device="cuda")
+        nat.check(self._lib.ts_dominant_gaussians(self.plan.handle, int(view), nat.dptr(gid),
+                                                  nat.dptr(dep), nat.stream_ptr(stream)),
+                  "ts_dominant_gaussians")
+        return gid, dep

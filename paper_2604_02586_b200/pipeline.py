@@ -1,0 +1,211 @@
+"""Motion-compensation entry point (gausstrack/pipeline.py:32-129) on the fused GPU path.
+
+`compensate_frame` keeps the reference signature.  Its four hot-path stages (rasterize,
+accumulate, per-view solve, multi-view fuse: pipeline.py:117-124 and :79-86) run as
+K1 -> K2 -> K3 -> K4 on the device without materialising weight maps or per-view objects.
+The reference's regularisation (kNN median filter, static pinning, propagation,
+regularize.py:37-188) is outside this build's scope; pass `regularize=` to plug it
+in (e.g. `gausstrack_regularizer()` when the reference package is importable).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .config import Config
+from .core import Gaussian3D, cameras_array, gaussians_array
+from .errors import DimensionMismatch, InvalidConfig
+from .motion2d import Status, ViewAccumulators, ViewMotionList
+from .multiview import MotionUpdateList
+
+
+@dataclass(frozen=True)
+class Clip:
+    first_frame: int
+    target_frames: tuple
+    views: tuple
+
+
+@dataclass
+class FrameResult:
+    frame: int
+    gaussians: list
+    tallies: dict
+    wall_time: dict
+    compensated_from: int | None = None
+
+
+class GaussianList:
+    """Array-backed, lazily materialised list[Gaussian3D] (rows: (N, 11) float64)."""
+
+    def __init__(self, rows):
+        self.rows = np.ascontiguousarray(rows, np.float64).reshape(-1, 11)
+
+    def __len__(self):
+        return len(self.rows)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        r = self.rows[i]
+        return Gaussian3D(r[0:3], r[3:7], r[7:10], r[10])
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
+def segment_clips(n_frames, clip_len, n_views, mode="short"):
+    """Short mode: disjoint blocks re-seeded from ground truth; long mode: chained blocks
+    sharing boundary frames (pipeline.py:48-72)."""
+    if clip_len < 2:
+        raise InvalidConfig(f"clip_len must be >= 2, got {clip_len}")
+    if mode not in ("short", "long"):
+        raise InvalidConfig(f"mode must be short|long, got {mode!r}")
+    views = tuple(range(n_views))
+    clips = []
+    if mode == "short":
+        for first in range(0, n_frames, clip_len):
+            last = min(first + clip_len, n_frames)
+            clips.append(Clip(first, tuple(range(first + 1, last)), views))
+        return clips
+    first = 0
+    while first < n_frames - 1:
+        last = min(first + clip_len - 1, n_frames - 1)
+        clips.append(Clip(first, tuple(range(first + 1, last + 1)), views))
+        first = last
+    return clips
+
+
+def apply_update_rows(rows, delta, rotation, scale, status):
+    """apply_updates (regularize.py:179-188) on arrays: unsolvable rows keep frame-1 values."""
+    out = np.array(rows, np.float64, copy=True).reshape(-1, 11)
+    keep = np.asarray(status) != 0
+    out[keep, 0:3] += delta[keep]
+    out[keep, 3:7] = rotation[keep]
+    out[keep, 7:10] = scale[keep]
+    return out
+
+
+def _tracks_arrays(tracks, n_views):
+    """Stack TrackField objects (or pass (V,H,W,2)/(V,H,W) arrays through)."""
+    if isinstance(tracks, tuple) and len(tracks) == 2:
+        return tracks
+    if len(tracks) != n_views:
+        raise DimensionMismatch("track fields and cameras count differ")
+    target = np.stack([np.asarray(t.target) for t in tracks])
+    valid = np.stack([np.asarray(t.valid, bool) for t in tracks]).astype(np.uint8)
+    if np.all(target[valid.astype(bool)] == target[valid.astype(bool)].astype(np.float32)):
+        target = target.astype(np.float32)  # TRKF-exact values: ship 4-byte targets
+    return target, valid
+
+
+_ENGINES = {}
+
+
+def _engine():
+    import torch
+
+    from .engine import FrameEngine
+    dev = torch.cuda.current_device()
+    if dev not in _ENGINES:
+        _ENGINES[dev] = FrameEngine()
+    return _ENGINES[dev]
+
+
+def compensate_frame(frame1, cameras, tracks, config: Config = None, weightmaps=None, knn=None,
+                     frame_index=0, first_frame_index=0, regularize=None) -> FrameResult:
+    """Single-frame motion compensation from first-frame Gaussians and per-view tracks.
+
+    Without `weightmaps` this is the fused GPU path; with them it runs the GPU stage kernels on
+    the given weight maps (as the reference skips its rasterizer).  `regularize(frame1, updates,
+    accs, config, knn) -> updates` optionally applies a regularisation stage.
+    """
+    config = config or Config()
+    t0 = time.perf_counter()
+    rows = gaussians_array(frame1)
+    cams = cameras_array(cameras)
+    n, nv = len(rows), len(cams)
+    if weightmaps is None:
+        eng = _engine()
+        eng.bin(rows, cams, config)
+        target, valid = _tracks_arrays(tracks, nv)
+        out = eng.compensate(target, valid)
+        import torch
+        torch.cuda.synchronize()
+        status = out.status.cpu().numpy()
+        updates = MotionUpdateList(out.delta_mean.cpu().numpy(), out.rotation.cpu().numpy(),
+                                   out.scale.cpu().numpy(), status)
+        ms = out.motion_status.cpu().numpy().reshape(nv, n)
+        ma = out.motion_a.cpu().numpy().reshape(nv, n, 2, 2)
+        mb = out.motion_b.cpu().numpy().reshape(nv, n, 2)
+        mw = out.weight_sum.cpu().numpy().reshape(nv, n)
+        mc = out.pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
+        msc = out.static_pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
+        msw = out.static_weight_sum.cpu().numpy().reshape(nv, n)
+        motions = [ViewMotionList(v, ms[v], ma[v], mb[v], mw[v], mc[v]) for v in range(nv)]
+        accs = [ViewAccumulators(v, None, None, mw[v], mc[v], msc[v], msw[v]) for v in range(nv)]
+    else:
+        from .motion2d import accumulate_view, solve_view
+        from .multiview import update_all
+        accs = [accumulate_view(wm, tf, n, config.static_threshold_px)
+                for wm, tf in zip(weightmaps, tracks)]
+        motions = [solve_view(a, config.det_floor, config.min_pixels, config.min_weight)
+                   for a in accs]
+        updates = update_all(rows, motions, cams, config.min_views, config.min_total_weight,
+                             config.min_total_pixels, config.eig_floor)
+    if regularize is not None:
+        updates = regularize(frame1, updates, accs, config, knn)
+    if isinstance(updates, MotionUpdateList):
+        new_rows = apply_update_rows(rows, updates.delta_mean, updates.rotation, updates.scale,
+                                     updates.status)
+        st = updates.status
+        tallies = {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
+                   "unsolvable": int((st == 0).sum())}
+    else:
+        delta = np.array([u.delta_mean for u in updates]).reshape(n, 3)
+        rot = np.array([u.new_rotation for u in updates]).reshape(n, 4)
+        sc = np.array([u.new_scale for u in updates]).reshape(n, 3)
+        st = np.array([{Status.UNSOLVABLE: 0, Status.SOLVED: 1, Status.STATIC: 2}[u.status]
+                       for u in updates], np.int8)
+        new_rows = apply_update_rows(rows, delta, rot, sc, st)
+        tallies = {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
+                   "unsolvable": int((st == 0).sum())}
+    dt = time.perf_counter() - t0
+    return FrameResult(frame_index, GaussianList(new_rows), tallies,
+                       {"tracking": 0.0, "compensation": dt, "refinement": 0.0},
+                       compensated_from=first_frame_index)
+
+
+def gausstrack_regularizer():
+    """A `regularize` hook that runs the reference package's CPU regularisation
+    (pipeline.py:88-98) on our updates, if `gausstrack` is importable."""
+    import gausstrack.regularize as reg
+    from gausstrack.motion2d import Status as RefStatus
+    from gausstrack.multiview import MotionUpdate as RefUpdate
+
+    ref_status = {0: RefStatus.UNSOLVABLE, 1: RefStatus.SOLVED, 2: RefStatus.STATIC}
+
+    def run(frame1, updates, accs, config, knn):
+        import gausstrack.core as gcore
+        rows = gaussians_array(frame1)
+        ref_frame = [gcore.Gaussian3D(r[0:3], r[3:7], r[7:10], r[10]) for r in rows]
+        if knn is None:
+            knn = reg.build_knn(rows[:, 0:3], config.knn_k)
+        ups = [RefUpdate(i, updates.delta_mean[i], updates.rotation[i], updates.scale[i],
+                         ref_status[int(updates.status[i])]) for i in range(len(rows))]
+        pc = np.stack([a.pixel_count for a in accs], axis=1)
+        sc = np.stack([a.static_pixel_count for a in accs], axis=1)
+        flags = reg.detect_static_all(pc, sc, config.min_hit_pixels, config.static_fraction,
+                                      config.min_views)
+        ups = reg.median_filter(ups, knn, ref_frame)
+        ups = reg.propagate(ups, knn, flags, ref_frame, config.propagation_average)
+        code = {RefStatus.UNSOLVABLE: 0, RefStatus.SOLVED: 1, RefStatus.STATIC: 2}
+        return MotionUpdateList(np.array([u.delta_mean for u in ups]),
+                                np.array([u.new_rotation for u in ups]),
+                                np.array([u.new_scale for u in ups]),
+                                np.array([code[u.status] for u in ups], np.int8))
+
+    return run
