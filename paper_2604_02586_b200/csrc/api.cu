@@ -55,7 +55,7 @@ enum Stage { ST_PROJECT = 0, ST_DEPTH_SORT, ST_TILE_SORT, ST_RASTER, ST_SOLVE, S
 struct ts_plan {
   // binning state
   DevBuf cams, rec, dkey, dkey2, dval, dval2, depth64, ntiles, status, bbox, cnt_sorted, off_sorted,
-      inst_base, tkey, tkey2, tval, tval2, range, cub_tmp;
+      inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf partial, flag, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt, mot_sw;
   // stage-API buffers
@@ -106,7 +106,7 @@ int64_t sum_workspace(const ts_plan *p) {
   const DevBuf *bufs[] = {&p->cams, &p->rec, &p->dkey, &p->dkey2, &p->dval, &p->dval2, &p->depth64,
                           &p->ntiles, &p->status, &p->bbox, &p->cnt_sorted, &p->off_sorted,
                           &p->inst_base, &p->tkey, &p->tkey2, &p->tval, &p->tval2, &p->range,
-                          &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a,
+                          &p->items, &p->counters, &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a,
                           &p->mot_b, &p->mot_w, &p->mot_cnt, &p->mot_scnt, &p->mot_sw,
                           &p->emit_count, &p->emit_key, &p->emit_key2, &p->emit_gv,
                           &p->emit_alpha, &p->emit_trans, &p->emit_idx, &p->emit_idx2,
@@ -121,7 +121,7 @@ void release_all(ts_plan *p) {
   DevBuf *bufs[] = {&p->cams, &p->rec, &p->dkey, &p->dkey2, &p->dval, &p->dval2, &p->depth64,
                     &p->ntiles, &p->status, &p->bbox, &p->cnt_sorted, &p->off_sorted,
                     &p->inst_base, &p->tkey, &p->tkey2, &p->tval, &p->tval2, &p->range,
-                    &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a, &p->mot_b,
+                    &p->items, &p->counters, &p->cub_tmp, &p->partial, &p->flag, &p->mot_status, &p->mot_a, &p->mot_b,
                     &p->mot_w, &p->mot_cnt, &p->mot_scnt, &p->mot_sw, &p->emit_count,
                     &p->emit_key, &p->emit_key2, &p->emit_gv, &p->emit_alpha, &p->emit_trans,
                     &p->emit_idx, &p->emit_idx2, &p->deg_flags, &p->deg_ids, &p->deg_count,
@@ -221,6 +221,8 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->inst_base, 4 * NV);
   const int64_t ntile_total = (int64_t)p->tpv * V;
   ENSURE(p->range, 8 * ntile_total);
+  ENSURE(p->items, 4 * (ntile_total + 1));
+  ENSURE(p->counters, 64);
 
   cudaEvent_t e0 = p->mark_begin(s);
   launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec), ptr<uint64_t>(p->dkey),
@@ -391,8 +393,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!p || !updates || p->V < 1) return TS_E_INVALID_ARGUMENT;
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
   const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
-  ENSURE(p->partial, sizeof(Partial) * (ni + 1));
-  ENSURE(p->flag, ni + 1);
+  ENSURE(p->partial, sizeof(Partial) * 4 * (ni + 1));
+  ENSURE(p->flag, 4 * (ni + 1));
   ts_motions m = motions ? *motions : ts_motions{};
   ts_motions im;
   {
@@ -412,10 +414,11 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   cudaEvent_t e3 = p->mark_begin(s);
-  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ni + 1, s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, 4 * (ni + 1), s));
   TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
-                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), track_target,
-                        track_valid, n, p->W, p->H, p->tiles_x, p->tpv, p->tpv * p->V, 0, p->cfg,
+                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
+                        ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,
+                        track_target, track_valid, p->W, p->H, p->tiles_x, p->tpv, p->cfg,
                         ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, s));
   p->mark_end(ST_RASTER, e3, s);
@@ -484,8 +487,9 @@ int ts_rasterize_weights(ts_plan *p, const double *gaussians, int64_t n, const t
     ENSURE(p->emit_count, 8);
     TS_CUDA_TRY(cudaMemsetAsync(p->emit_count.p, 0, 8, s));
     TS_CUDA_TRY(launch_k2(K2_EMIT, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
-                          ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), nullptr, nullptr, n,
-                          p->W, p->H, p->tiles_x, p->tpv, p->tpv, 0, cfg, nullptr, nullptr,
+                          ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
+                          ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv, nullptr,
+                          nullptr, p->W, p->H, p->tiles_x, p->tpv, cfg, nullptr, nullptr,
                           ptr<unsigned long long>(p->emit_count), cap, ptr<uint64_t>(p->emit_key),
                           ptr<uint32_t>(p->emit_gv), ptr<double>(p->emit_alpha),
                           ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, s));
@@ -650,9 +654,10 @@ int ts_dominant_gaussians(ts_plan *p, int32_t view, int64_t *gid_img, double *de
   TS_CUDA_TRY(cudaMemsetAsync(gid_img, 0xFF, 8 * (size_t)p->W * p->H, s));
   TS_CUDA_TRY(cudaMemsetAsync(depth_img, 0, 8 * (size_t)p->W * p->H, s));
   TS_CUDA_TRY(launch_k2(K2_DOMINANT, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
-                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base), nullptr, nullptr,
-                        p->n, p->W, p->H, p->tiles_x, p->tpv, p->tpv, view * p->tpv, p->cfg,
-                        nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
+                        ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
+                        ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), view * p->tpv,
+                        (view + 1) * p->tpv, nullptr, nullptr, p->W, p->H, p->tiles_x, p->tpv,
+                        p->cfg, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
                         ptr<double>(p->depth64), gid_img, depth_img, s));
   return TS_OK;
 }

@@ -22,10 +22,10 @@ void launch_project_view(const double *G, int64_t n, const ts_camera &cam, doubl
                          double *depth, double *cov2, uint8_t *in_front, cudaStream_t s);
 
 cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uint32_t *inst_gv,
-                      const uint32_t *tile_range, const uint32_t *inst_base,
-                      const void *track_target, const uint8_t *track_valid, int64_t n, int W,
-                      int H, int tiles_x, int tiles_per_view, int n_tiles_total,
-                      int tile_offset, const ts_config &cfg, Partial *partial, uint8_t *flag,
+                      const uint32_t *tile_range, const uint32_t *inst_base, uint32_t *items,
+                      uint32_t *counters, int tile_begin, int tile_end, const void *track_target,
+                      const uint8_t *track_valid, int W, int H, int tiles_x, int tiles_per_view,
+                      const ts_config &cfg, Partial *partial, uint8_t *flag,
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,

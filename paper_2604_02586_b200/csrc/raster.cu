@@ -3,50 +3,49 @@
 // Reference semantics: gausstrack/splat.py:147-195 (alpha, keep predicate, per-pixel
 // front-to-back transmittance, early stop) fused with motion2d.py:144-160 (accumulate_view).
 //
-// One CTA (256 threads, 8 warps) per 16x16 tile; warp w owns the 8x4 pixel block
-// ((w&1)*8, (w>>1)*4) and lane l the pixel (l&7, l>>3) inside it.  The tile's Gaussian list is
-// already in (depth, gid) order (K1), so each lane walks it front to back exactly as the
-// reference walks a pixel's sorted contributions.
-//   * Batches of K2_BATCH records are staged in shared memory (64-byte records).
-//   * Warp-level culling: for every chunk of 32 records, one ballot of "bbox intersects my 8x4
-//     block" leaves only the Gaussians that can touch the warp's pixels; warps whose pixels are
-//     all saturated (T < early_stop) skip work, and the CTA stops once every pixel saturated.
+// Work decomposition.  K1 bins Gaussians into 16x16-pixel tiles, each tile's list in the
+// reference order (depth, gid).  K2 is a persistent kernel whose WARPS are independent: a warp
+// pulls a work item (tile, quadrant) from a global atomic queue, owns that 8x8-pixel quadrant
+// (lane l holds pixels l and l+32, two independent fp64 chains for ILP) and walks the tile list
+// front to back.  No block barrier anywhere: a warp stops as soon as its 64 pixels are saturated
+// (T < early_stop) and takes the next item, so occluded Gaussians cost almost nothing.
+//   * Culling: per 32-instance chunk, each lane loads one record and a single ballot of
+//     "bbox intersects my quadrant" selects the Gaussians this warp has to evaluate.
 //   * Predicates in fp64 in the reference's operation order (bit-exact q and alpha >= cutoff;
 //     T >= early_stop up to the reference's own log-cumsum rounding).
-//   * Accumulation is transposed instead of shuffled: a contributing lane stores w = alpha*T
-//     into a per-warp 32x32 shared buffer; after the chunk, lane j sums Gaussian j's
-//     contributions over the warp's 32 pixels (no shuffles) into a per-warp partial.  The CTA then
-//     adds the 8 warp partials IN WARP ORDER and writes ONE partial per (tile, Gaussian) instance
-//     to its own slot -- no atomics of any kind, no zero-initialised accumulators, and results
-//     that are bit-reproducible run to run (K3 adds a Gaussian's tile partials in instance order).
+//   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp
+//     [16 x 64] shared buffer; every 16 evaluated Gaussians, lane l sums Gaussian (l & 15)'s
+//     contributions over pixel half (l >> 4) in pixel order, one xor-16 shuffle step adds the
+//     halves, and the partial moments go to the (instance, quadrant) sub-slot: no atomics, no
+//     zero-initialised accumulators, bit-reproducible (K3 adds the sub-slots in fixed order).
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace ts {
 
-constexpr int K2_THREADS = 256;
-constexpr int K2_WARPS = K2_THREADS / 32;
-constexpr int K2_BATCH = 128;
-constexpr int K2_WROW = 33;     // padded row of the per-warp w buffer (bank spread)
-constexpr int K2_PSTRIDE = 15;  // per-warp partial: 13 moments, count, static count
+constexpr int K2_WARPS = 4;     // warps per CTA (independent; shared memory partitioned)
+constexpr int K2_FLUSH = 16;    // evaluated Gaussians per transposed reduction
+constexpr int K2_WROW = 65;     // padded row of the w buffer (64 pixels)
 
 struct K2Params {
   const RasterRec *rec;
   const uint32_t *inst_gv;     // sorted instances: gv
   const uint32_t *tile_range;  // [start, end) per global tile
-  const uint32_t *inst_base;   // per gv: first partial slot (gv order scan of tile counts)
+  const uint32_t *inst_base;   // per gv: first instance slot (gv-order scan of tile counts)
+  const uint32_t *items;       // non-empty global tile ids
+  const uint32_t *n_items;     // device count of items
+  uint32_t *work_counter;      // zeroed before launch
   const void *track_target;    // (V, H, W, 2)
   const uint8_t *track_valid;  // (V, H, W)
-  int64_t n;                   // Gaussians
-  int W, H, tiles_x, tiles_per_view, tile_offset;
+  int W, H, tiles_x, tiles_per_view;
   double alpha_cutoff, early_stop, static_thr;
   // accumulate mode
-  Partial *partial;
+  Partial *partial;  // 4 sub-slots (quadrants) per instance
   uint8_t *flag;
   // emit mode
   unsigned long long *emit_count;
   int64_t emit_cap;
-  uint64_t *emit_key;   // (pixel << 32) | sequence number within the pixel
+  uint64_t *emit_key;  // (pixel << 32) | sequence number within the pixel
   uint32_t *emit_gv;
   double *emit_alpha, *emit_trans;
   // dominant mode
@@ -55,243 +54,309 @@ struct K2Params {
   double *dom_depth;
 };
 
-struct K2Smem {
-  RasterRec rec[K2_BATCH];
-  uint32_t slot[K2_BATCH];
-  double trk_u[K2_THREADS];
-  double trk_v[K2_THREADS];
-  uint8_t trk_static[K2_THREADS];
-  double w[K2_WARPS][32][K2_WROW];
-  double part[K2_WARPS][32][K2_PSTRIDE];
+struct K2Warp {
+  RasterRec rec[32];
+  uint32_t slot[32];
+  double w[K2_FLUSH][K2_WROW];
+  double trk_u[64], trk_v[64];
+  uint8_t trk_static[64];
 };
 
+// One pixel of a lane: predicate evaluation and front-to-back compositing (splat.py:147-193).
+struct PixelState {
+  double T;
+  bool done;
+};
+
+__device__ __forceinline__ bool eval_pixel(const RasterRec &r, int px, int py, double cutoff,
+                                           double early_stop, PixelState &ps, double &a_out,
+                                           double &w_out, double &tin_out) {
+  if (ps.done || px < r.x0 || px > r.x1 || py < r.y0 || py > r.y1) return false;
+  const double dx = sub((double)px, r.mx), dy = sub((double)py, r.my);
+  const double q = mahalanobis(r, dx, dy);
+  if (!(q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS)) return false;
+  const double a = alpha_of(r.opacity, q);
+  if (!(a >= cutoff)) return false;
+  const double tin = ps.T;
+  w_out = mul(a, tin);  // motion2d.py:151
+  ps.T = mul(tin, sub(1.0, a));
+  if (!(ps.T >= early_stop)) ps.done = true;
+  a_out = a;
+  tin_out = tin;
+  return true;
+}
+
 template <int MODE, typename TrackT>
-__global__ void __launch_bounds__(K2_THREADS, 2) k2_raster(const K2Params P) {
+__global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-  K2Smem &S = *reinterpret_cast<K2Smem *>(k2_smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  K2Warp &S = reinterpret_cast<K2Warp *>(k2_smem_raw)[warp];
+  const uint32_t n_units = 4u * *P.n_items;
 
-  const int tile = blockIdx.x + P.tile_offset;
-  const uint32_t start = P.tile_range[2 * tile], end = P.tile_range[2 * tile + 1];
-  if (start >= end) return;
-  const int v = tile / P.tiles_per_view;
-  const int t = tile - v * P.tiles_per_view;
-  const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
+  for (;;) {
+    uint32_t unit = 0;
+    if (lane == 0) unit = atomicAdd(P.work_counter, 1u);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= n_units) break;
+    const int tile = (int)P.items[unit >> 2];
+    const int quad = (int)(unit & 3);
+    const uint32_t start = P.tile_range[2 * tile], end = P.tile_range[2 * tile + 1];
+    const int v = tile / P.tiles_per_view;
+    const int t = tile - v * P.tiles_per_view;
+    const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
+    const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 4 * 2;
+    // lane pixels: p0 = lane (rows 0-3), p1 = lane + 32 (rows 4-7) of the 8x8 quadrant
+    const int px = qx0 + (lane & 7);
+    const int py0 = qy0 + (lane >> 3), py1 = py0 + 4;
+    const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rx0 = tx * TS_TILE + (warp & 1) * 8, ry0 = ty * TS_TILE + (warp >> 1) * 4;
-  const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
-  const bool inimg = px < P.W && py < P.H;
-
-  // per-pixel track (motion2d.py:145-150) and static flag (motion2d.py:158)
-  bool valid = false;
-  if (MODE == K2_ACCUMULATE) {
-    double u = 0.0, vv = 0.0;
-    if (inimg) {
-      const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
-      valid = P.track_valid[pix] != 0;
-      if (valid) {
-        const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
-        u = load_track(tg);
-        vv = load_track(tg + 1);
-      }
-    }
-    S.trk_u[tid] = u;
-    S.trk_v[tid] = vv;
-    S.trk_static[tid] = valid && is_static(u, vv, px, py, P.static_thr);
-  }
-  double T = 1.0;
-  bool done = !inimg || !(T >= P.early_stop);
-  uint32_t seq = 0;  // emit mode: contribution index within the pixel
-  double best_w = -1.0;  // dominant mode
-  uint32_t best_gv = 0xFFFFFFFFu, best_g = 0xFFFFFFFFu;
-
-  for (uint32_t b = start; b < end; b += K2_BATCH) {
-    // CTA-uniform early exit; also the barrier protecting the shared batch buffers
-    if (__syncthreads_count(!done) == 0) break;
-    const int nb = min((int)(end - b), K2_BATCH);
-    if (tid < nb) {
-      const uint32_t gv = P.inst_gv[b + tid];
-      const RasterRec r = P.rec[gv];
-      S.rec[tid] = r;
-      if (MODE == K2_ACCUMULATE) {
-        const int tx0 = r.x0 / TS_TILE, tx1 = r.x1 / TS_TILE, ty0 = r.y0 / TS_TILE;
-        S.slot[tid] = P.inst_base[gv] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
-      } else {
-        S.slot[tid] = gv;
-      }
-    }
-    __syncthreads();
-
-    for (int c = 0; c < nb; c += 32) {
-      uint32_t my_cmask = 0;
-      if (!__all_sync(0xffffffffu, done)) {
-        // warp-level culling: which of these 32 records touch this warp's 8x4 block?
-        bool hit = false;
-        if (c + lane < nb) {
-          const RasterRec &r = S.rec[c + lane];
-          hit = !(r.x1 < rx0 || r.x0 > rx0 + 7 || r.y1 < ry0 || r.y0 > ry0 + 3);
+    bool valid0 = false, valid1 = false;
+    if (MODE == K2_ACCUMULATE) {
+      double u[2] = {0.0, 0.0}, vv[2] = {0.0, 0.0};
+      bool val[2] = {false, false};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int py = h ? py1 : py0;
+        if (h ? in1 : in0) {
+          const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
+          val[h] = P.track_valid[pix] != 0;
+          if (val[h]) {
+            const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
+            u[h] = load_track(tg);
+            vv[h] = load_track(tg + 1);
+          }
         }
-        uint32_t mask = __ballot_sync(0xffffffffu, hit);
-        while (mask) {
+        const int p = lane + 32 * h;
+        S.trk_u[p] = u[h];
+        S.trk_v[p] = vv[h];
+        S.trk_static[p] = val[h] && is_static(u[h], vv[h], px, py, P.static_thr);
+      }
+      valid0 = val[0];
+      valid1 = val[1];
+    }
+    PixelState s0{1.0, !in0 || !(1.0 >= P.early_stop)};
+    PixelState s1{1.0, !in1 || !(1.0 >= P.early_stop)};
+    uint32_t seq0 = 0, seq1 = 0;                  // emit mode
+    double best_w0 = -1.0, best_w1 = -1.0;        // dominant mode
+    uint32_t best_g0 = 0xFFFFFFFFu, best_g1 = 0xFFFFFFFFu, best_gv0 = 0, best_gv1 = 0;
+
+    for (uint32_t b = start; b < end; b += 32) {
+      if (__all_sync(0xffffffffu, s0.done && s1.done)) break;
+      // load + cull 32 instances
+      const uint32_t i = b + lane;
+      bool hit = false;
+      __syncwarp();
+      if (i < end) {
+        const uint32_t gv = P.inst_gv[i];
+        const RasterRec r = P.rec[gv];
+        hit = !(r.x1 < qx0 || r.x0 > qx0 + 7 || r.y1 < qy0 || r.y0 > qy0 + 7);
+        if (hit) {
+          S.rec[lane] = r;
+          if (MODE == K2_ACCUMULATE) {
+            const int tx0 = r.x0 / TS_TILE, tx1 = r.x1 / TS_TILE, ty0 = r.y0 / TS_TILE;
+            S.slot[lane] = 4u * (P.inst_base[gv] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) +
+                                                             (tx - tx0))) + (uint32_t)quad;
+          } else {
+            S.slot[lane] = gv;
+          }
+        }
+      }
+      uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      __syncwarp();
+      while (mask) {
+        // evaluate up to K2_FLUSH hitting Gaussians in depth order
+        uint32_t my_cm = 0;
+        int my_j = 0;
+        int k = 0;
+        for (; k < K2_FLUSH && mask; k++) {
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
-          const RasterRec &r = S.rec[c + j];
-          bool contrib = false;
-          if (!done && px >= r.x0 && px <= r.x1 && py >= r.y0 && py <= r.y1) {
-            const double dx = sub((double)px, r.mx), dy = sub((double)py, r.my);
-            const double q = mahalanobis(r, dx, dy);
-            if (q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS) {
-              const double a = alpha_of(r.opacity, q);
-              if (a >= P.alpha_cutoff) {
-                const double tin = T;
-                const double w = mul(a, tin);  // motion2d.py:151
-                T = mul(tin, sub(1.0, a));
-                if (!(T >= P.early_stop)) done = true;
-                if (MODE == K2_ACCUMULATE) {
-                  contrib = valid;
-                  if (contrib) S.w[warp][j][lane] = w;
-                } else if (MODE == K2_EMIT) {
-                  const unsigned long long idx = atomicAdd(P.emit_count, 1ull);
-                  if ((int64_t)idx < P.emit_cap) {
-                    P.emit_key[idx] = ((uint64_t)((uint32_t)(py * P.W + px)) << 32) | seq;
-                    P.emit_gv[idx] = S.slot[c + j];
-                    P.emit_alpha[idx] = a;
-                    P.emit_trans[idx] = tin;
-                  }
-                  seq++;
-                } else {  // K2_DOMINANT: argmax alpha*T, ties by smaller id (scene.py:179)
-                  const uint32_t g = r.g;
-                  if (w > best_w || (w == best_w && g < best_g)) {
-                    best_w = w;
-                    best_gv = S.slot[c + j];
-                    best_g = g;
-                  }
-                }
+          const RasterRec &r = S.rec[j];
+          double a0 = 0, w0 = 0, t0 = 0, a1 = 0, w1 = 0, t1 = 0;
+          const bool c0 = eval_pixel(r, px, py0, P.alpha_cutoff, P.early_stop, s0, a0, w0, t0);
+          const bool c1 = eval_pixel(r, px, py1, P.alpha_cutoff, P.early_stop, s1, a1, w1, t1);
+          if (MODE == K2_ACCUMULATE) {
+            const bool k0 = c0 && valid0, k1 = c1 && valid1;
+            if (k0) S.w[k][lane] = w0;
+            if (k1) S.w[k][lane + 32] = w1;
+            const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
+            const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
+            if (lane == k) {
+              my_cm = cm0;
+              my_j = j;
+            }
+            if (lane == k + 16) {
+              my_cm = cm1;
+              my_j = j;
+            }
+          } else if (MODE == K2_EMIT) {
+            if (c0 || c1) {
+              const unsigned long long idx = atomicAdd(P.emit_count, (unsigned long long)(c0 + c1));
+              unsigned long long o = idx;
+              if (c0 && (int64_t)o < P.emit_cap) {
+                P.emit_key[o] = ((uint64_t)((uint32_t)(py0 * P.W + px)) << 32) | seq0;
+                P.emit_gv[o] = S.slot[j];
+                P.emit_alpha[o] = a0;
+                P.emit_trans[o] = t0;
+              }
+              if (c0) o++;
+              if (c1 && (int64_t)o < P.emit_cap) {
+                P.emit_key[o] = ((uint64_t)((uint32_t)(py1 * P.W + px)) << 32) | seq1;
+                P.emit_gv[o] = S.slot[j];
+                P.emit_alpha[o] = a1;
+                P.emit_trans[o] = t1;
               }
             }
-          }
-          if (MODE == K2_ACCUMULATE) {
-            const uint32_t cm = __ballot_sync(0xffffffffu, contrib);
-            if (lane == j) my_cmask = cm;
-          }
-        }
-      }
-      if (MODE == K2_ACCUMULATE) {
-        __syncwarp();
-        // lane `lane` owns record c+lane: sum its contributions over this warp's pixels,
-        // in pixel order, relative to the Gaussian's integer anchor
-        double m[TS_NMOM];
-#pragma unroll
-        for (int k = 0; k < TS_NMOM; k++) m[k] = 0.0;
-        uint32_t cnt = 0, scnt = 0;
-        if (my_cmask) {
-          const RasterRec &r = S.rec[c + lane];
-          const double ax = (double)anchor_x(r), ay = (double)anchor_y(r);
-          uint32_t bits = my_cmask;
-          while (bits) {
-            const int p = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const double w = S.w[warp][lane][p];
-            const int pt = warp * 32 + p;
-            const double dx = (double)(rx0 + (p & 7)) - ax, dy = (double)(ry0 + (p >> 3)) - ay;
-            const double ua = S.trk_u[pt] - ax, va = S.trk_v[pt] - ay;
-            const double wx = w * dx, wy = w * dy;
-            m[0] += w;
-            m[1] += wx;
-            m[2] += wy;
-            m[3] += wx * dx;
-            m[4] += wx * dy;
-            m[5] += wy * dy;
-            m[6] += w * ua;
-            m[7] += w * va;
-            m[8] += wx * ua;
-            m[9] += wx * va;
-            m[10] += wy * ua;
-            m[11] += wy * va;
-            if (S.trk_static[pt]) {
-              m[12] += w;
-              scnt++;
+            seq0 += c0;
+            seq1 += c1;
+          } else {  // K2_DOMINANT: argmax alpha*T, ties by smaller id (scene.py:179)
+            const uint32_t g = r.g;
+            if (c0 && (w0 > best_w0 || (w0 == best_w0 && g < best_g0))) {
+              best_w0 = w0;
+              best_g0 = g;
+              best_gv0 = S.slot[j];
             }
-            cnt++;
+            if (c1 && (w1 > best_w1 || (w1 == best_w1 && g < best_g1))) {
+              best_w1 = w1;
+              best_g1 = g;
+              best_gv1 = S.slot[j];
+            }
           }
         }
+        if (MODE == K2_ACCUMULATE) {
+          __syncwarp();
+          if (__any_sync(0xffffffffu, my_cm != 0)) {
+            // lane: Gaussian kk = lane & 15 of this flush, pixel half hh = lane >> 4
+            const int kk = lane & 15, hh = lane >> 4;
+            double m[TS_NMOM];
 #pragma unroll
-        for (int k = 0; k < TS_NMOM; k++) S.part[warp][lane][k] = m[k];
-        S.part[warp][lane][13] = (double)cnt;
-        S.part[warp][lane][14] = (double)scnt;
-        __syncthreads();
-        // fixed-order cross-warp reduction: thread -> (record j, field k)
-        for (int task = tid; task < 32 * 16; task += K2_THREADS) {
-          const int j = task >> 4, k = task & 15;
-          if (c + j >= nb) continue;
-          double tot_cnt = 0.0;
+            for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
+            uint32_t cnt = 0, scnt = 0;
+            if (my_cm) {
+              const RasterRec &r = S.rec[my_j];
+              const double ax = (double)anchor_x(r), ay = (double)anchor_y(r);
+              uint32_t bits = my_cm;
+              while (bits) {
+                const int p = __ffs(bits) - 1 + 32 * hh;
+                bits &= bits - 1;
+                const double w = S.w[kk][p];
+                const double dx = (double)(qx0 + (p & 7)) - ax, dy = (double)(qy0 + (p >> 3)) - ay;
+                const double ua = S.trk_u[p] - ax, va = S.trk_v[p] - ay;
+                const double wx = w * dx, wy = w * dy;
+                m[0] += w;
+                m[1] += wx;
+                m[2] += wy;
+                m[3] += wx * dx;
+                m[4] += wx * dy;
+                m[5] += wy * dy;
+                m[6] += w * ua;
+                m[7] += w * va;
+                m[8] += wx * ua;
+                m[9] += wx * va;
+                m[10] += wy * ua;
+                m[11] += wy * va;
+                if (S.trk_static[p]) {
+                  m[12] += w;
+                  scnt++;
+                }
+                cnt++;
+              }
+            }
+            // add the upper half (pixels 32..63) into the lower half lanes, fixed order
 #pragma unroll
-          for (int ww = 0; ww < K2_WARPS; ww++) tot_cnt += S.part[ww][j][13];
-          if (tot_cnt == 0.0) continue;
-          Partial *dst = P.partial + S.slot[c + j];
-          if (k < TS_NMOM) {
-            double s = 0.0;
+            for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_down_sync(0xffffffffu, m[q], 16);
+            cnt += __shfl_down_sync(0xffffffffu, cnt, 16);
+            scnt += __shfl_down_sync(0xffffffffu, scnt, 16);
+            const int jj = __shfl_down_sync(0xffffffffu, my_j, 16);
+            if (hh == 0 && kk < k && cnt > 0) {
+              const int jsel = my_cm ? my_j : jj;
+              const uint32_t slot = S.slot[jsel];
+              Partial *dst = P.partial + slot;
 #pragma unroll
-            for (int ww = 0; ww < K2_WARPS; ww++) s += S.part[ww][j][k];
-            dst->m[k] = s;
-          } else if (k == 13) {
-            double s = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < K2_WARPS; ww++) s += S.part[ww][j][14];
-            dst->count = (uint32_t)tot_cnt;
-            dst->static_count = (uint32_t)s;
-          } else {
-            P.flag[S.slot[c + j]] = 1;
+              for (int q = 0; q < TS_NMOM; q++) dst->m[q] = m[q];
+              dst->count = cnt;
+              dst->static_count = scnt;
+              P.flag[slot] = 1;
+            }
           }
+          __syncwarp();
         }
-        __syncthreads();
       }
     }
-  }
-  if (MODE == K2_DOMINANT && inimg) {
-    const int64_t pix = (int64_t)py * P.W + px;
-    if (best_gv != 0xFFFFFFFFu) {
-      P.dom_gid[pix] = best_g;
-      P.dom_depth[pix] = P.depth64[best_gv];
-    } else {
-      P.dom_gid[pix] = -1;
-      P.dom_depth[pix] = 0.0;
+    if (MODE == K2_DOMINANT) {
+      if (in0) {
+        const int64_t pix = (int64_t)py0 * P.W + px;
+        P.dom_gid[pix] = best_g0 != 0xFFFFFFFFu ? (int64_t)best_g0 : -1;
+        P.dom_depth[pix] = best_g0 != 0xFFFFFFFFu ? P.depth64[best_gv0] : 0.0;
+      }
+      if (in1) {
+        const int64_t pix = (int64_t)py1 * P.W + px;
+        P.dom_gid[pix] = best_g1 != 0xFFFFFFFFu ? (int64_t)best_g1 : -1;
+        P.dom_depth[pix] = best_g1 != 0xFFFFFFFFu ? P.depth64[best_gv1] : 0.0;
+      }
     }
   }
 }
 
+// Compact list of the non-empty tiles in [t0, t1) (order irrelevant: every unit is independent).
+__global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, int t1,
+                               uint32_t *__restrict__ items, uint32_t *__restrict__ n_items) {
+  const int t = t0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ne = t < t1 && tile_range[2 * t] < tile_range[2 * t + 1];
+  const uint32_t m = __ballot_sync(0xffffffffu, ne);
+  if (!m) return;
+  uint32_t base = 0;
+  const int lane = threadIdx.x & 31;
+  if (lane == __ffs(m) - 1) base = atomicAdd(n_items, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (ne) items[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)t;
+}
+
 template <int MODE, typename TrackT>
-static cudaError_t launch_mode(const K2Params &P, int n_tiles, cudaStream_t s) {
+static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
   auto kern = k2_raster<MODE, TrackT>;
-  const size_t smem = sizeof(K2Smem);
+  const size_t smem = sizeof(K2Warp) * K2_WARPS;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_tiles > 0) kern<<<n_tiles, K2_THREADS, smem, s>>>(P);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<sms * (per_sm > 0 ? per_sm : 1), K2_WARPS * 32, smem, s>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uint32_t *inst_gv,
-                      const uint32_t *tile_range, const uint32_t *inst_base,
-                      const void *track_target, const uint8_t *track_valid, int64_t n, int W,
-                      int H, int tiles_x, int tiles_per_view, int n_tiles_total,
-                      int tile_offset, const ts_config &cfg, Partial *partial, uint8_t *flag,
+                      const uint32_t *tile_range, const uint32_t *inst_base, uint32_t *items,
+                      uint32_t *counters, int tile_begin, int tile_end, const void *track_target,
+                      const uint8_t *track_valid, int W, int H, int tiles_x, int tiles_per_view,
+                      const ts_config &cfg, Partial *partial, uint8_t *flag,
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
                       cudaStream_t s) {
+  // counters[0] = number of items, counters[1] = work queue head
+  cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const int nt = tile_end - tile_begin;
+  if (nt > 0)
+    k2_build_items<<<(nt + 255) / 256, 256, 0, s>>>(tile_range, tile_begin, tile_end, items,
+                                                    counters);
   K2Params P;
   P.rec = rec;
   P.inst_gv = inst_gv;
   P.tile_range = tile_range;
   P.inst_base = inst_base;
+  P.items = items;
+  P.n_items = counters;
+  P.work_counter = counters + 1;
   P.track_target = track_target;
   P.track_valid = track_valid;
-  P.n = n;
   P.W = W;
   P.H = H;
   P.tiles_x = tiles_x;
   P.tiles_per_view = tiles_per_view;
-  P.tile_offset = tile_offset;
   P.alpha_cutoff = cfg.alpha_cutoff;
   P.early_stop = cfg.early_stop;
   P.static_thr = cfg.static_threshold_px;
@@ -307,11 +372,11 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.dom_gid = dom_gid;
   P.dom_depth = dom_depth;
   if (mode == K2_ACCUMULATE) {
-    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, n_tiles_total, s);
-    return launch_mode<K2_ACCUMULATE, double>(P, n_tiles_total, s);
+    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s);
+    return launch_mode<K2_ACCUMULATE, double>(P, s);
   }
-  if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, n_tiles_total, s);
-  return launch_mode<K2_DOMINANT, float>(P, n_tiles_total, s);
+  if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s);
+  return launch_mode<K2_DOMINANT, float>(P, s);
 }
 
 }  // namespace ts

@@ -18,9 +18,10 @@ TS_HD void qr_add_row(double (&R)[N][N], double (&row)[N]) {
     const double bb = row[k];
     if (bb == 0.0) continue;
     const double a = R[k][k];
-    const double r = hypot(a, bb);
-    const double c = a / r, s = bb / r;
-    R[k][k] = r;
+    const double rr = fma(a, a, bb * bb);
+    const double inv = rsqrt(rr);
+    const double c = a * inv, s = bb * inv;
+    R[k][k] = rr * inv;
 #pragma unroll
     for (int j = k + 1; j < N; j++) {
       const double t = R[k][j];
@@ -38,9 +39,10 @@ TS_HD void qr_add_row_rhs(double (&R)[N][N], double (&c6)[N],
     const double bb = row[k];
     if (bb == 0.0) continue;
     const double a = R[k][k];
-    const double r = hypot(a, bb);
-    const double c = a / r, s = bb / r;
-    R[k][k] = r;
+    const double rr = fma(a, a, bb * bb);
+    const double inv = rsqrt(rr);
+    const double c = a * inv, s = bb * inv;
+    R[k][k] = rr * inv;
 #pragma unroll
     for (int j = k + 1; j < N; j++) {
       const double t = R[k][j];
@@ -80,7 +82,7 @@ TS_HD void jacobi_svd(double (&B)[N][N], double (&V)[N][N], double (&s)[N]) {
         rotated = true;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        const double c = 1.0 / sqrt(fma(t, t, 1.0));
+        const double c = rsqrt(fma(t, t, 1.0));
         const double sn = c * t;
 #pragma unroll
         for (int i = 0; i < N; i++) {
@@ -154,7 +156,36 @@ TS_HD bool triangulate_from_r(const double (&R)[4][4], double *mean) {
 // solve_covariance3d from R (6x6) and Q^T b (multiview.py:259-263).
 TS_HD bool cov_from_r(const double (&R)[6][6], const double (&c6)[6],
                                            double *sol) {
+  // Rigorous cheap bound first: s_max <= |R|_F and s_min >= 1/|R^-1|_F, so
+  // 1/(|R|_F |R^-1|_F) >= 1e-9 proves the reference's rank test passes; only otherwise run the
+  // one-sided Jacobi SVD to take the exact decision.
+  bool need_svd = false;
   {
+    double fro = 0.0, finv = 0.0;
+    double Ri[6][6];
+#pragma unroll
+    for (int i = 0; i < 6; i++)
+#pragma unroll
+      for (int j = i; j < 6; j++) fro = fma(R[i][j], R[i][j], fro);
+#pragma unroll
+    for (int i = 0; i < 6; i++) need_svd = need_svd || !(R[i][i] != 0.0);
+    if (!need_svd) {
+      // column j of R^-1 by back substitution on e_j
+#pragma unroll
+      for (int j = 0; j < 6; j++) {
+#pragma unroll
+        for (int i = 5; i >= 0; i--) {
+          double acc = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+          for (int k = i + 1; k < 6; k++) acc -= R[i][k] * Ri[k][j];
+          Ri[i][j] = (i <= j) ? acc / R[i][i] : 0.0;
+          finv = fma(Ri[i][j], Ri[i][j], finv);
+        }
+      }
+      need_svd = !(1.0 >= 1.0000001 * TS_SINGULAR_GAP_REL * sqrt(fro * finv));
+    }
+  }
+  if (need_svd) {
     double B[6][6], s[6];
     double Vd[6][6];
 #pragma unroll
@@ -204,7 +235,7 @@ TS_HD void eigh3(double (&A)[3][3], double (&E)[3][3], double (&ev)[3]) {
         rotated = true;
         const double theta = (aqq - app) / (2.0 * apq);
         const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
-        const double c = 1.0 / sqrt(fma(t, t, 1.0));
+        const double c = rsqrt(fma(t, t, 1.0));
         const double s = t * c;
         const int r = 3 - p - q;  // the third index
         const double arp = A[r][p], arq = A[r][q];

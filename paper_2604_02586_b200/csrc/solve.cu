@@ -95,8 +95,9 @@ __global__ void __launch_bounds__(256) k3_solve(const Partial *__restrict__ part
   uint32_t cnt = 0, scnt = 0;
   double ax = 0.0, ay = 0.0;
   if (nt) {
-    const uint32_t base = inst_base[gv];
-    for (uint32_t i = 0; i < nt; i++) {
+    // 4 quadrant sub-slots per (tile, Gaussian) instance, added in fixed order
+    const uint32_t base = 4u * inst_base[gv];
+    for (uint32_t i = 0; i < 4u * nt; i++) {
       if (!flag[base + i]) continue;
       const Partial &p = partial[base + i];
 #pragma unroll
