@@ -179,6 +179,24 @@ TS_HD double mahalanobis(const RasterRec &r, double dx, double dy) {
 }
 
 // alpha = min(o * exp(-0.5 q), 0.999)  (splat.py:154)
+// Table-driven exp(-q/2) for q in [0, 9] (the only range alpha is needed in):
+// exp(x) = E[k] * P6(r), k = rint(64 x), r = x - k/64, |r| <= 1/128, E[k] = exp(-k/64).
+// <= 2 ulp (vs numpy's exp: rel <= 5e-16); 11 instructions instead of the general exp.
+#define TS_EXP_TABLE 289
+TS_HD double alpha_of_table(double opacity, double q, const double *etab) {
+  const double x = mul(-0.5, q);
+  const double kf = rint(x * 64.0);
+  const double r = fma(kf, -0.015625, x);
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(r, p, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = fma(r, p, 1.0);
+  const double a = mul(opacity, etab[(int)(-kf)] * p);
+  return a > TS_ALPHA_CLAMP ? TS_ALPHA_CLAMP : a;
+}
+
 TS_HD double alpha_of(double opacity, double q) {
   double a = mul(opacity, exp(mul(-0.5, q)));
   return a > TS_ALPHA_CLAMP ? TS_ALPHA_CLAMP : a;

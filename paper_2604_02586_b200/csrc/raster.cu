@@ -56,11 +56,23 @@ struct K2Params {
 
 struct K2Warp {
   RasterRec rec[32];
+  uint64_t rect[32];  // bbox of the record clipped to the quadrant, as a 64-pixel bit mask
   uint32_t slot[32];
   double w[K2_FLUSH][K2_WROW];
   double trk_u[64], trk_v[64];
   uint8_t trk_static[64];
 };
+
+// 64-bit mask (bit = row * 8 + col) of the quadrant pixels inside the record's bbox.
+__device__ __forceinline__ uint64_t quad_rect(const RasterRec &r, int qx0, int qy0) {
+  const int cx0 = max((int)r.x0 - qx0, 0), cx1 = min((int)r.x1 - qx0, 7);
+  const int cy0 = max((int)r.y0 - qy0, 0), cy1 = min((int)r.y1 - qy0, 7);
+  if (cx0 > cx1 || cy0 > cy1) return 0ull;
+  const uint64_t cols = (uint64_t)((0xFFu >> (7 - cx1)) & (0xFFu << cx0) & 0xFFu);
+  const uint64_t hi = cy1 == 7 ? ~0ull : ((1ull << (8 * (cy1 + 1))) - 1ull);
+  const uint64_t lo = (1ull << (8 * cy0)) - 1ull;
+  return (cols * 0x0101010101010101ull) & hi & ~lo;
+}
 
 // One pixel of a lane: predicate evaluation and front-to-back compositing (splat.py:147-193).
 struct PixelState {
@@ -68,14 +80,15 @@ struct PixelState {
   bool done;
 };
 
-__device__ __forceinline__ bool eval_pixel(const RasterRec &r, int px, int py, double cutoff,
-                                           double early_stop, PixelState &ps, double &a_out,
-                                           double &w_out, double &tin_out) {
-  if (ps.done || px < r.x0 || px > r.x1 || py < r.y0 || py > r.y1) return false;
+__device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, int px, int py,
+                                           double cutoff, double early_stop, const double *etab,
+                                           PixelState &ps, double &a_out, double &w_out,
+                                           double &tin_out) {
+  if (!cand) return false;  // outside the bbox, or already saturated
   const double dx = sub((double)px, r.mx), dy = sub((double)py, r.my);
   const double q = mahalanobis(r, dx, dy);
   if (!(q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS)) return false;
-  const double a = alpha_of(r.opacity, q);
+  const double a = alpha_of_table(r.opacity, q, etab);
   if (!(a >= cutoff)) return false;
   const double tin = ps.T;
   w_out = mul(a, tin);  // motion2d.py:151
@@ -89,6 +102,9 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, int px, int py, d
 template <int MODE, typename TrackT>
 __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
+  __shared__ double etab[TS_EXP_TABLE];  // exp(-k/64), k = 0..288
+  for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   K2Warp &S = reinterpret_cast<K2Warp *>(k2_smem_raw)[warp];
   const uint32_t n_units = 4u * *P.n_items;
@@ -140,18 +156,23 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
     double best_w0 = -1.0, best_w1 = -1.0;        // dominant mode
     uint32_t best_g0 = 0xFFFFFFFFu, best_g1 = 0xFFFFFFFFu, best_gv0 = 0, best_gv1 = 0;
 
+    // saturated pixels of the quadrant (bit = row * 8 + col), warp-uniform
+    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
+                      ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
     for (uint32_t b = start; b < end; b += 32) {
-      if (__all_sync(0xffffffffu, s0.done && s1.done)) break;
-      // load + cull 32 instances
+      if (done64 == ~0ull) break;
+      // load + cull 32 instances: keep Gaussians whose bbox covers an unsaturated pixel
       const uint32_t i = b + lane;
       bool hit = false;
       __syncwarp();
       if (i < end) {
         const uint32_t gv = P.inst_gv[i];
         const RasterRec r = P.rec[gv];
-        hit = !(r.x1 < qx0 || r.x0 > qx0 + 7 || r.y1 < qy0 || r.y0 > qy0 + 7);
+        const uint64_t rect = quad_rect(r, qx0, qy0);
+        hit = (rect & ~done64) != 0ull;
         if (hit) {
           S.rec[lane] = r;
+          S.rect[lane] = rect;
           if (MODE == K2_ACCUMULATE) {
             const int tx0 = r.x0 / TS_TILE, tx1 = r.x1 / TS_TILE, ty0 = r.y0 / TS_TILE;
             S.slot[lane] = 4u * (P.inst_base[gv] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) +
@@ -168,13 +189,20 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
         uint32_t my_cm = 0;
         int my_j = 0;
         int k = 0;
-        for (; k < K2_FLUSH && mask; k++) {
+        while (k < K2_FLUSH && mask) {
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
-          const RasterRec &r = S.rec[j];
+          // warp-uniform skip of Gaussians that only cover saturated pixels
+          const uint64_t cand = S.rect[j] & ~done64;
+          if (cand == 0ull) continue;
+          const RasterRec r = S.rec[j];
           double a0 = 0, w0 = 0, t0 = 0, a1 = 0, w1 = 0, t1 = 0;
-          const bool c0 = eval_pixel(r, px, py0, P.alpha_cutoff, P.early_stop, s0, a0, w0, t0);
-          const bool c1 = eval_pixel(r, px, py1, P.alpha_cutoff, P.early_stop, s1, a1, w1, t1);
+          const bool c0 = eval_pixel(r, (cand >> lane) & 1ull, px, py0, P.alpha_cutoff,
+                                     P.early_stop, etab, s0, a0, w0, t0);
+          const bool c1 = eval_pixel(r, (cand >> (lane + 32)) & 1ull, px, py1, P.alpha_cutoff,
+                                     P.early_stop, etab, s1, a1, w1, t1);
+          done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
+                   ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
           if (MODE == K2_ACCUMULATE) {
             const bool k0 = c0 && valid0, k1 = c1 && valid1;
             if (k0) S.w[k][lane] = w0;
@@ -222,6 +250,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
               best_gv1 = S.slot[j];
             }
           }
+          k++;
         }
         if (MODE == K2_ACCUMULATE) {
           __syncwarp();
