@@ -31,6 +31,13 @@ class Status(enum.Enum):
 
 STATUS_CODE = {Status.UNSOLVABLE: 0, Status.SOLVED: 1, Status.STATIC: 2}
 CODE_STATUS = {v: k for k, v in STATUS_CODE.items()}
+_VALUE_CODE = {"unsolvable": 0, "solved": 1, "static": 2}
+
+
+def status_code(status):
+    """Integer status of a Status member -- ours or the reference's (matched by value, so
+    gausstrack.motion2d.Status objects are accepted as well)."""
+    return _VALUE_CODE.get(getattr(status, "value", status), 0)
 
 
 @dataclass
@@ -131,7 +138,7 @@ def motions_arrays(vms):
     if isinstance(vms, ViewMotionList):
         return vms.status, vms.a, vms.b, vms.weight_sum, vms.pixel_count
     n = len(vms)
-    status = np.array([STATUS_CODE.get(vm.status, 0) for vm in vms], np.int8).reshape(n)
+    status = np.array([status_code(vm.status) for vm in vms], np.int8).reshape(n)
     a = np.array([vm.motion.a for vm in vms], np.float64).reshape(n, 2, 2)
     b = np.array([vm.motion.b for vm in vms], np.float64).reshape(n, 2)
     w = np.array([vm.weight_sum for vm in vms], np.float64).reshape(n)

@@ -17,7 +17,7 @@ from . import _native as nat
 from .core import Gaussian2D, Sym3, cameras_array, gaussians_array
 from .errors import (DegenerateGeometry, InsufficientViews, NegativeEigenvalue,
                      RankDeficient)
-from .motion2d import Status, motions_arrays
+from .motion2d import Status, motions_arrays, status_code
 
 MIN_VIEWS_DEFAULT = 2
 MIN_TOTAL_WEIGHT_DEFAULT = 1e-3
@@ -223,7 +223,7 @@ def update_gaussian(g, view_motions, views, gaussian_id=-1, min_views=MIN_VIEWS_
     w = np.zeros((nv, 1))
     c = np.zeros((nv, 1), np.int64)
     for vm in view_motions:
-        if vm.status != Status.SOLVED:
+        if status_code(vm.status) != 1:
             continue
         v = vm.view_id
         st[v, 0] = 1

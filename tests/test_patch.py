@@ -1,0 +1,58 @@
+"""patch.install() rebinds the reference pipeline's stage names (CPU: mechanics and type
+conversion only; skipped where the reference package is not importable)."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture(scope="module")
+def gausstrack():
+    if not os.path.isdir(REF):
+        pytest.skip("reference package not present")
+    sys.path.insert(0, REF)
+    try:
+        import gausstrack
+        return gausstrack
+    finally:
+        sys.path.remove(REF)
+
+
+def test_install_rebinds_pipeline_names(gausstrack):
+    import gausstrack.pipeline as gp
+    import gausstrack.scene as gs
+
+    from paper_2604_02586_b200 import patch
+    before = {n: getattr(gp, n) for n in patch._STAGES}
+    h = patch.install()
+    try:
+        for n in patch._STAGES:
+            assert getattr(gp, n) is not before[n]
+            assert getattr(gp, n).__module__ == "paper_2604_02586_b200.patch"
+        assert gs.rasterize_weights.__module__ == "paper_2604_02586_b200.patch"
+    finally:
+        patch.uninstall(h)
+    for n in patch._STAGES:
+        assert getattr(gp, n) is before[n]
+
+
+def test_reference_typed_motions(gausstrack):
+    import gausstrack.core as gcore
+    import gausstrack.motion2d as gm
+
+    from paper_2604_02586_b200.motion2d import ViewMotionList, motions_arrays
+    from paper_2604_02586_b200.patch import to_reference_motions
+    vml = ViewMotionList(2, [1, 0, 1], np.tile(np.eye(2), (3, 1, 1)) * 1.5,
+                         np.arange(6.0).reshape(3, 2), [1.0, 0.0, 2.0], [4, 0, 9])
+    ref = to_reference_motions(vml, gm, gcore)
+    assert [vm.status for vm in ref] == [gm.Status.SOLVED, gm.Status.UNSOLVABLE,
+                                         gm.Status.SOLVED]
+    assert isinstance(ref[0].motion, gcore.AffineMotion) and ref[1].view_id == 2
+    # our array extraction accepts the reference's enum (matched by value)
+    st, a, b, w, c = motions_arrays(ref)
+    np.testing.assert_array_equal(st, [1, 0, 1])
+    np.testing.assert_array_equal(b[2], [4.0, 5.0])
