@@ -5,6 +5,8 @@
 // (instance count after binning, contribution count of the emitting rasterizer).
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -57,6 +59,7 @@ struct ts_plan {
   DevBuf cams, rec, dkey, dkey2, dval, dval2, depth64, ntiles, status, bbox, cnt_sorted, off_sorted,
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
+  DevBuf k2_stats;
   DevBuf partial, flag, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt, mot_sw;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
@@ -191,6 +194,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
               const ts_config *cfg, cudaStream_t s) {
   int rc = validate_cams(cams, V);
   if (rc) return rc;
+  if (V > 64) return TS_E_INVALID_ARGUMENT;  // 6 view bits in the 32-bit depth key
   if (n < 0 || (uint64_t)n * (uint64_t)V >= 0xFFFFFFFFull) return TS_E_INVALID_ARGUMENT;
   p->n = n;
   p->V = V;
@@ -208,8 +212,8 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->cams, sizeof(ts_camera) * V);
   TS_CUDA_TRY(cudaMemcpyAsync(p->cams.p, cams, sizeof(ts_camera) * V, cudaMemcpyHostToDevice, s));
   ENSURE(p->rec, sizeof(RasterRec) * NV);
-  ENSURE(p->dkey, 8 * NV);
-  ENSURE(p->dkey2, 8 * NV);
+  ENSURE(p->dkey, 4 * NV);
+  ENSURE(p->dkey2, 4 * NV);
   ENSURE(p->dval, 4 * NV);
   ENSURE(p->dval2, 4 * NV);
   ENSURE(p->depth64, 8 * NV);
@@ -225,7 +229,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->counters, 64);
 
   cudaEvent_t e0 = p->mark_begin(s);
-  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec), ptr<uint64_t>(p->dkey),
+  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->dkey),
                     ptr<uint32_t>(p->dval), ptr<double>(p->depth64), ptr<uint32_t>(p->ntiles),
                     ptr<int8_t>(p->status), ptr<int16_t>(p->bbox), s);
   TS_CUDA_TRY(cudaGetLastError());
@@ -233,13 +237,13 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
 
   cudaEvent_t e1 = p->mark_begin(s);
   if (NV > 0) {
-    const int end_bit = 32 + bits_for((uint64_t)V);
+    const int end_bit = 26 + bits_for((uint64_t)V);
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
-      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint64_t>(p->dkey),
-                                             ptr<uint64_t>(p->dkey2), ptr<uint32_t>(p->dval),
+      return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint32_t>(p->dkey),
+                                             ptr<uint32_t>(p->dkey2), ptr<uint32_t>(p->dval),
                                              ptr<uint32_t>(p->dval2), (int)NV, 0, end_bit, s);
     }));
-    launch_k1_fix_ties(ptr<uint64_t>(p->dkey2), ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
+    launch_k1_fix_ties(ptr<uint32_t>(p->dkey2), ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
                        s);
     launch_k1_gather_counts(ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->ntiles),
                             ptr<uint32_t>(p->cnt_sorted), NV, s);
@@ -284,6 +288,26 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_TILE_SORT, e2, s);
   return TS_OK;
+}
+
+// Debug: TS_K2_STATS=1 makes ts_frame_compensate print K2's work counters to stderr.
+unsigned long long *k2_stats(ts_plan *p, cudaStream_t s) {
+  static const bool on = getenv("TS_K2_STATS") != nullptr;
+  if (!on) return nullptr;
+  if (p->k2_stats.ensure(16 * 8, s) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(p->k2_stats.p, 0, 16 * 8, s);
+  return p->k2_stats.as<unsigned long long>();
+}
+
+void k2_stats_report(ts_plan *p, cudaStream_t s) {
+  static const bool on = getenv("TS_K2_STATS") != nullptr;
+  if (!on || !p->k2_stats.p) return;
+  unsigned long long h[16];
+  cudaMemcpyAsync(h, p->k2_stats.p, 9 * 8, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  fprintf(stderr, "K2 stats: units %llu chunks %llu instances %llu hits %llu skips %llu "
+          "eval_gauss %llu eval_pix %llu contrib %llu flushes %llu\n", h[0], h[1], h[2], h[3],
+          h[4], h[5], h[6], h[7], h[8]);
 }
 
 ts_motions internal_motions(ts_plan *p) {
@@ -420,12 +444,15 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,
                         track_target, track_valid, p->W, p->H, p->tiles_x, p->tpv, p->cfg,
                         ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
-                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, s));
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, k2_stats(p, s), s));
+  k2_stats_report(p, s);
   p->mark_end(ST_RASTER, e3, s);
 
+  // K3 and K4 stay separate: a fused per-Gaussian K3+K4 serialises the memory-bound per-view
+  // fits inside a 200-register thread and measured 3.0 ms vs 0.6 + 1.5 ms (cfg2).
   cudaEvent_t e4 = p->mark_begin(s);
   launch_k3_solve(ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), ptr<uint32_t>(p->inst_base),
-                  ptr<uint32_t>(p->ntiles), ptr<RasterRec>(p->rec), NV, p->cfg, m, s);
+                  ptr<uint32_t>(p->ntiles), ptr<int16_t>(p->bbox), NV, p->cfg, m, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 
@@ -492,7 +519,7 @@ int ts_rasterize_weights(ts_plan *p, const double *gaussians, int64_t n, const t
                           nullptr, p->W, p->H, p->tiles_x, p->tpv, cfg, nullptr, nullptr,
                           ptr<unsigned long long>(p->emit_count), cap, ptr<uint64_t>(p->emit_key),
                           ptr<uint32_t>(p->emit_gv), ptr<double>(p->emit_alpha),
-                          ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, s));
+                          ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, nullptr, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, p->emit_count.p, 8, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 2, p->deg_count.p, 8, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
@@ -658,7 +685,7 @@ int ts_dominant_gaussians(ts_plan *p, int32_t view, int64_t *gid_img, double *de
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), view * p->tpv,
                         (view + 1) * p->tpv, nullptr, nullptr, p->W, p->H, p->tiles_x, p->tpv,
                         p->cfg, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
-                        ptr<double>(p->depth64), gid_img, depth_img, s));
+                        ptr<double>(p->depth64), gid_img, depth_img, nullptr, s));
   return TS_OK;
 }
 

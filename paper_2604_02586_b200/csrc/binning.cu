@@ -5,11 +5,11 @@
 // tile's Gaussian list by the same key, so every pixel of the tile sees its Gaussians in exactly
 // the reference order:
 //   1. k1_project: one thread per Gaussian, looping over the V cameras (the 88-byte Gaussian is
-//      read once): writes the 64-byte RasterRec, a 64-bit sort key (view << 32 | f32(depth) bits)
-//      and the tile count of its bbox.
-//   2. CUB radix sort by that key (37 bits at V=20).  f32 rounding is monotone, so the order is
-//      right except inside runs of equal f32 depth; k1_fix_ties re-sorts those (short) runs by
-//      the exact (f64 depth, gid) key.
+//      read once): writes the 64-byte RasterRec, a 32-bit sort key (view << 26 | top 26 bits of
+//      the positive f32 depth) and the tile count of its bbox.
+//   2. CUB radix sort by that key (31 bits at V=20, 4 passes).  Rounding to f32 and dropping low
+//      mantissa bits are monotone, so the order is right except inside runs of equal keys;
+//      k1_fix_ties re-sorts those (short) runs by the exact (f64 depth, gid) key.
 //   3. k1_emit writes one (tile, gv) instance per covered tile in that depth order; a stable CUB
 //      radix sort on the tile id alone then yields tile-major, depth-ordered lists.
 //   4. k1_tile_ranges marks [start, end) of every tile.
@@ -21,7 +21,7 @@ namespace ts {
 __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, int64_t n,
                                                   const ts_camera *__restrict__ cams, int V,
                                                   RasterRec *__restrict__ rec,
-                                                  uint64_t *__restrict__ dkey,
+                                                  uint32_t *__restrict__ dkey,
                                                   uint32_t *__restrict__ dval,
                                                   double *__restrict__ depth64,
                                                   uint32_t *__restrict__ ntiles,
@@ -45,18 +45,18 @@ __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, 
     int st = footprint(p, gs[10], cam.width, cam.height, r);
     int64_t gv = (int64_t)v * n + g;
     status[gv] = (int8_t)st;
-    uint64_t key = ((uint64_t)v << 32);
+    uint32_t key = ((uint32_t)v << 26);
     uint32_t nt = 0;
     int16_t bb[4] = {0, -1, 0, -1};
     if (st == 3) {
       r.g = (uint32_t)g;
       r.pad = 0;
       rec[gv] = r;
-      key |= (uint64_t)__float_as_uint(__double2float_rn(p.depth));
+      key |= __float_as_uint(__double2float_rn(p.depth)) >> 5;  // depth > 0: < 0x3FC0000
       nt = (uint32_t)((r.x1 / TS_TILE - r.x0 / TS_TILE + 1) * (r.y1 / TS_TILE - r.y0 / TS_TILE + 1));
       bb[0] = r.x0; bb[1] = r.x1; bb[2] = r.y0; bb[3] = r.y1;
     } else {
-      key |= 0xFFFFFFFFull;  // sorts after every binned Gaussian of the view, never emitted
+      key |= 0x3FFFFFFu;  // sorts after every binned Gaussian of the view, never emitted
     }
     dkey[gv] = key;
     dval[gv] = (uint32_t)gv;
@@ -67,12 +67,12 @@ __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, 
 }
 
 // Re-sort runs of equal (view, f32 depth) keys by the exact (f64 depth, gid) key.
-__global__ void k1_fix_ties(const uint64_t *__restrict__ key, uint32_t *__restrict__ val,
+__global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restrict__ val,
                             const double *__restrict__ depth64, int64_t M) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= M) return;
-  uint64_t kk = key[k];
-  if ((uint32_t)kk == 0xFFFFFFFFu) return;
+  const uint32_t kk = key[k];
+  if ((kk & 0x3FFFFFFu) == 0x3FFFFFFu) return;
   if (k > 0 && key[k - 1] == kk) return;
   if (k + 1 >= M || key[k + 1] != kk) return;
   int64_t e = k + 1;
@@ -153,13 +153,13 @@ __global__ void k_project_view(const double *__restrict__ G, int64_t n, ts_camer
 static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint64_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
+                       uint32_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
                        int8_t *status, int16_t *bbox, cudaStream_t s) {
   if (n == 0) return;
   k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, dkey, dval,
                                                                   depth64, ntiles, status, bbox);
 }
-void launch_k1_fix_ties(const uint64_t *key, uint32_t *val, const double *depth64, int64_t M,
+void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         cudaStream_t s) {
   if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M);
 }

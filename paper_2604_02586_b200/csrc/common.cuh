@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <cstring>
 
 #include "../../include/trackersplat_b200.h"
 
@@ -183,9 +184,21 @@ TS_HD double mahalanobis(const RasterRec &r, double dx, double dy) {
 // exp(x) = E[k] * P6(r), k = rint(64 x), r = x - k/64, |r| <= 1/128, E[k] = exp(-k/64).
 // <= 2 ulp (vs numpy's exp: rel <= 5e-16); 11 instructions instead of the general exp.
 #define TS_EXP_TABLE 289
+// low 32 bits of a double as an int (the integer n of a 1.5*2^52-shifted value)
+TS_HD int lo_int(double d) {
+#ifdef __CUDA_ARCH__
+  return __double2loint(d);
+#else
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return (int)(uint32_t)u;
+#endif
+}
 TS_HD double alpha_of_table(double opacity, double q, const double *etab) {
   const double x = mul(-0.5, q);
-  const double kf = rint(x * 64.0);
+  // round-to-nearest-even of 64 x with the 1.5*2^52 shifter: stays on the fp64 pipe (no F2F/F2I)
+  const double kd = fma(x, 64.0, 6755399441055744.0);
+  const double kf = kd - 6755399441055744.0;
   const double r = fma(kf, -0.015625, x);
   double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
   p = fma(r, p, 1.0 / 24.0);
@@ -193,7 +206,7 @@ TS_HD double alpha_of_table(double opacity, double q, const double *etab) {
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);
-  const double a = mul(opacity, etab[(int)(-kf)] * p);
+  const double a = mul(opacity, etab[-lo_int(kd)] * p);
   return a > TS_ALPHA_CLAMP ? TS_ALPHA_CLAMP : a;
 }
 

@@ -19,7 +19,7 @@
 namespace ts {
 
 
-__global__ void __launch_bounds__(128) k4_fuse(const double *__restrict__ G, int64_t n,
+__global__ void __launch_bounds__(128, 3) k4_fuse(const double *__restrict__ G, int64_t n,
                                                const ts_camera *__restrict__ cams, int V,
                                                ts_motions m, ts_config cfg, ts_updates u) {
   extern __shared__ ts_camera s_cam4[];

@@ -8,9 +8,9 @@ namespace ts {
 enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
 
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint64_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
+                       uint32_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
                        int8_t *status, int16_t *bbox, cudaStream_t s);
-void launch_k1_fix_ties(const uint64_t *key, uint32_t *val, const double *depth64, int64_t M,
+void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         cudaStream_t s);
 void launch_k1_gather_counts(const uint32_t *val, const uint32_t *ntiles, uint32_t *cnt_sorted,
                              int64_t M, cudaStream_t s);
@@ -29,11 +29,11 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      cudaStream_t s);
+                      unsigned long long *stats, cudaStream_t s);
 
 // K3: per-(view, Gaussian) affine fit from the tile partials of K2.
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
-                     const uint32_t *ntiles, const RasterRec *rec, int64_t nv_total,
+                     const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, cudaStream_t s);
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,

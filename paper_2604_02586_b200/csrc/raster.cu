@@ -7,24 +7,27 @@
 // reference order (depth, gid).  K2 is a persistent kernel whose WARPS are independent: a warp
 // pulls a work item (tile, quadrant) from a global atomic queue, owns that 8x8-pixel quadrant
 // (lane l holds pixels l and l+32, two independent fp64 chains for ILP) and walks the tile list
-// front to back.  No block barrier anywhere: a warp stops as soon as its 64 pixels are saturated
-// (T < early_stop) and takes the next item, so occluded Gaussians cost almost nothing.
-//   * Culling: per 32-instance chunk, each lane loads one record and a single ballot of
-//     "bbox intersects my quadrant" selects the Gaussians this warp has to evaluate.
+// front to back.  No block barrier in the main loop: a warp stops as soon as its 64 pixels are
+// saturated (T < early_stop) and takes the next item, so occluded Gaussians cost almost nothing.
+//   * Culling: per 32-instance chunk, each lane loads one record and computes the 64-bit mask of
+//     quadrant pixels inside its bbox; one ballot keeps the Gaussians whose mask meets an
+//     unsaturated pixel.  Per evaluated Gaussian the candidate mask (bbox AND NOT saturated) is
+//     re-checked warp-uniformly, so Gaussians over saturated pixels cost a few instructions.
 //   * Predicates in fp64 in the reference's operation order (bit-exact q and alpha >= cutoff;
 //     T >= early_stop up to the reference's own log-cumsum rounding).
-//   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp
-//     [16 x 64] shared buffer; every 16 evaluated Gaussians, lane l sums Gaussian (l & 15)'s
-//     contributions over pixel half (l >> 4) in pixel order, one xor-16 shuffle step adds the
-//     halves, and the partial moments go to the (instance, quadrant) sub-slot: no atomics, no
-//     zero-initialised accumulators, bit-reproducible (K3 adds the sub-slots in fixed order).
+//   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp [8 x 64]
+//     shared buffer; every 8 evaluated Gaussians, lane l sums Gaussian (l & 7)'s contributions
+//     over pixel quarter (l >> 3) in pixel order, two xor-shuffle steps add the quarters (exactly
+//     commutative pairs, so every lane holds the same bits), and the anchored moments go to the
+//     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
+//     bit-reproducible (K3 adds the sub-slots in fixed order).
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace ts {
 
 constexpr int K2_WARPS = 4;     // warps per CTA (independent; shared memory partitioned)
-constexpr int K2_FLUSH = 16;    // evaluated Gaussians per transposed reduction
+constexpr int K2_FLUSH = 8;     // evaluated Gaussians per transposed reduction
 constexpr int K2_WROW = 65;     // padded row of the w buffer (64 pixels)
 
 struct K2Params {
@@ -52,14 +55,20 @@ struct K2Params {
   const double *depth64;
   int64_t *dom_gid;
   double *dom_depth;
+  // optional work counters (debug; nullptr in production): see K2_STAT_*
+  unsigned long long *stats;
 };
 
+enum { K2S_UNITS, K2S_CHUNKS, K2S_INSTANCES, K2S_HITS, K2S_SKIPS, K2S_EVAL_GAUSS, K2S_EVAL_PIX,
+       K2S_CONTRIB, K2S_FLUSHES, K2S_N };
+
+template <typename TrackT>
 struct K2Warp {
   RasterRec rec[32];
   uint64_t rect[32];  // bbox of the record clipped to the quadrant, as a 64-pixel bit mask
   uint32_t slot[32];
   double w[K2_FLUSH][K2_WROW];
-  double trk_u[64], trk_v[64];
+  TrackT trk_u[64], trk_v[64];  // track targets in their input precision
   uint8_t trk_static[64];
 };
 
@@ -80,12 +89,12 @@ struct PixelState {
   bool done;
 };
 
-__device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, int px, int py,
+__device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double fpx, double fpy,
                                            double cutoff, double early_stop, const double *etab,
                                            PixelState &ps, double &a_out, double &w_out,
                                            double &tin_out) {
   if (!cand) return false;  // outside the bbox, or already saturated
-  const double dx = sub((double)px, r.mx), dy = sub((double)py, r.my);
+  const double dx = sub(fpx, r.mx), dy = sub(fpy, r.my);
   const double q = mahalanobis(r, dx, dy);
   if (!(q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS)) return false;
   const double a = alpha_of_table(r.opacity, q, etab);
@@ -100,14 +109,15 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, int px
 }
 
 template <int MODE, typename TrackT>
-__global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
+__global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
   __shared__ double etab[TS_EXP_TABLE];  // exp(-k/64), k = 0..288
   for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  K2Warp &S = reinterpret_cast<K2Warp *>(k2_smem_raw)[warp];
+  K2Warp<TrackT> &S = reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw)[warp];
   const uint32_t n_units = 4u * *P.n_items;
+  unsigned long long st[K2S_N] = {};
 
   for (;;) {
     uint32_t unit = 0;
@@ -120,35 +130,35 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
     const int v = tile / P.tiles_per_view;
     const int t = tile - v * P.tiles_per_view;
     const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
-    const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 4 * 2;
+    const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 8;
     // lane pixels: p0 = lane (rows 0-3), p1 = lane + 32 (rows 4-7) of the 8x8 quadrant
     const int px = qx0 + (lane & 7);
     const int py0 = qy0 + (lane >> 3), py1 = py0 + 4;
+    const double fpx = (double)px, fpy0 = (double)py0, fpy1 = (double)py1;
     const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
 
     bool valid0 = false, valid1 = false;
     if (MODE == K2_ACCUMULATE) {
-      double u[2] = {0.0, 0.0}, vv[2] = {0.0, 0.0};
-      bool val[2] = {false, false};
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int py = h ? py1 : py0;
+        TrackT u = TrackT(0), vv = TrackT(0);
+        bool val = false;
         if (h ? in1 : in0) {
           const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
-          val[h] = P.track_valid[pix] != 0;
-          if (val[h]) {
+          val = P.track_valid[pix] != 0;
+          if (val) {
             const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
-            u[h] = load_track(tg);
-            vv[h] = load_track(tg + 1);
+            u = __ldg(tg);
+            vv = __ldg(tg + 1);
           }
         }
         const int p = lane + 32 * h;
-        S.trk_u[p] = u[h];
-        S.trk_v[p] = vv[h];
-        S.trk_static[p] = val[h] && is_static(u[h], vv[h], px, py, P.static_thr);
+        S.trk_u[p] = u;
+        S.trk_v[p] = vv;
+        S.trk_static[p] = val && is_static((double)u, (double)vv, px, py, P.static_thr);
+        if (h) valid1 = val; else valid0 = val;
       }
-      valid0 = val[0];
-      valid1 = val[1];
     }
     PixelState s0{1.0, !in0 || !(1.0 >= P.early_stop)};
     PixelState s1{1.0, !in1 || !(1.0 >= P.early_stop)};
@@ -159,8 +169,13 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
     // saturated pixels of the quadrant (bit = row * 8 + col), warp-uniform
     uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
                       ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
+    if (P.stats) st[K2S_UNITS]++;
     for (uint32_t b = start; b < end; b += 32) {
       if (done64 == ~0ull) break;
+      if (P.stats) {
+        st[K2S_CHUNKS]++;
+        st[K2S_INSTANCES] += min(32u, end - b);
+      }
       // load + cull 32 instances: keep Gaussians whose bbox covers an unsaturated pixel
       const uint32_t i = b + lane;
       bool hit = false;
@@ -183,10 +198,11 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
         }
       }
       uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (P.stats) st[K2S_HITS] += __popc(mask);
       __syncwarp();
       while (mask) {
         // evaluate up to K2_FLUSH hitting Gaussians in depth order
-        uint32_t my_cm = 0;
+        uint32_t my_cm = 0;  // this lane's 16-pixel slice of its owned Gaussian's contributions
         int my_j = 0;
         int k = 0;
         while (k < K2_FLUSH && mask) {
@@ -194,12 +210,19 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
           mask &= mask - 1;
           // warp-uniform skip of Gaussians that only cover saturated pixels
           const uint64_t cand = S.rect[j] & ~done64;
-          if (cand == 0ull) continue;
+          if (cand == 0ull) {
+            if (P.stats) st[K2S_SKIPS]++;
+            continue;
+          }
+          if (P.stats) {
+            st[K2S_EVAL_GAUSS]++;
+            st[K2S_EVAL_PIX] += __popcll(cand);
+          }
           const RasterRec r = S.rec[j];
           double a0 = 0, w0 = 0, t0 = 0, a1 = 0, w1 = 0, t1 = 0;
-          const bool c0 = eval_pixel(r, (cand >> lane) & 1ull, px, py0, P.alpha_cutoff,
+          const bool c0 = eval_pixel(r, (cand >> lane) & 1ull, fpx, fpy0, P.alpha_cutoff,
                                      P.early_stop, etab, s0, a0, w0, t0);
-          const bool c1 = eval_pixel(r, (cand >> (lane + 32)) & 1ull, px, py1, P.alpha_cutoff,
+          const bool c1 = eval_pixel(r, (cand >> (lane + 32)) & 1ull, fpx, fpy1, P.alpha_cutoff,
                                      P.early_stop, etab, s1, a1, w1, t1);
           done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
                    ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
@@ -209,12 +232,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
             if (k1) S.w[k][lane + 32] = w1;
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
             const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
-            if (lane == k) {
-              my_cm = cm0;
-              my_j = j;
-            }
-            if (lane == k + 16) {
-              my_cm = cm1;
+            if (P.stats) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
+            if ((lane & 7) == k) {
+              const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
+              my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
               my_j = j;
             }
           } else if (MODE == K2_EMIT) {
@@ -255,22 +276,25 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
         if (MODE == K2_ACCUMULATE) {
           __syncwarp();
           if (__any_sync(0xffffffffu, my_cm != 0)) {
-            // lane: Gaussian kk = lane & 15 of this flush, pixel half hh = lane >> 4
-            const int kk = lane & 15, hh = lane >> 4;
+            if (P.stats) st[K2S_FLUSHES]++;
+            // lane: Gaussian kk = lane & 7 of this flush, pixel quarter qq = lane >> 3
+            const int kk = lane & 7, qq = lane >> 3;
             double m[TS_NMOM];
 #pragma unroll
             for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
             uint32_t cnt = 0, scnt = 0;
             if (my_cm) {
               const RasterRec &r = S.rec[my_j];
-              const double ax = (double)anchor_x(r), ay = (double)anchor_y(r);
+              const int axi = anchor_x(r), ayi = anchor_y(r);
+              const double ax = (double)axi, ay = (double)ayi;
+              const double bx = (double)(qx0 - axi), by = (double)(qy0 - ayi);
               uint32_t bits = my_cm;
               while (bits) {
-                const int p = __ffs(bits) - 1 + 32 * hh;
+                const int p = __ffs(bits) - 1 + 16 * qq;
                 bits &= bits - 1;
                 const double w = S.w[kk][p];
-                const double dx = (double)(qx0 + (p & 7)) - ax, dy = (double)(qy0 + (p >> 3)) - ay;
-                const double ua = S.trk_u[p] - ax, va = S.trk_v[p] - ay;
+                const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
+                const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
                 const double wx = w * dx, wy = w * dy;
                 m[0] += w;
                 m[1] += wx;
@@ -291,15 +315,19 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
                 cnt++;
               }
             }
-            // add the upper half (pixels 32..63) into the lower half lanes, fixed order
+            // add the four pixel quarters: (q0 + q1) + (q2 + q3) in every lane (commutative
+            // pairs, so all four lanes of a Gaussian hold identical bits)
 #pragma unroll
-            for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_down_sync(0xffffffffu, m[q], 16);
-            cnt += __shfl_down_sync(0xffffffffu, cnt, 16);
-            scnt += __shfl_down_sync(0xffffffffu, scnt, 16);
-            const int jj = __shfl_down_sync(0xffffffffu, my_j, 16);
-            if (hh == 0 && kk < k && cnt > 0) {
-              const int jsel = my_cm ? my_j : jj;
-              const uint32_t slot = S.slot[jsel];
+            for (int q = 0; q < TS_NMOM; q++) {
+              m[q] += __shfl_xor_sync(0xffffffffu, m[q], 8);
+              m[q] += __shfl_xor_sync(0xffffffffu, m[q], 16);
+            }
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
+            scnt += __shfl_xor_sync(0xffffffffu, scnt, 8);
+            scnt += __shfl_xor_sync(0xffffffffu, scnt, 16);
+            if (qq == 0 && kk < k && cnt > 0) {
+              const uint32_t slot = S.slot[my_j];
               Partial *dst = P.partial + slot;
 #pragma unroll
               for (int q = 0; q < TS_NMOM; q++) dst->m[q] = m[q];
@@ -325,6 +353,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32) k2_raster(const K2Params P) {
       }
     }
   }
+  if (P.stats && lane == 0)
+    for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);
 }
 
 // Compact list of the non-empty tiles in [t0, t1) (order irrelevant: every unit is independent).
@@ -344,7 +374,7 @@ __global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, 
 template <int MODE, typename TrackT>
 static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
   auto kern = k2_raster<MODE, TrackT>;
-  const size_t smem = sizeof(K2Warp) * K2_WARPS;
+  const size_t smem = sizeof(K2Warp<TrackT>) * K2_WARPS;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -364,7 +394,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      cudaStream_t s) {
+                      unsigned long long *stats, cudaStream_t s) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -400,6 +430,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.depth64 = depth64;
   P.dom_gid = dom_gid;
   P.dom_depth = dom_depth;
+  P.stats = stats;
   if (mode == K2_ACCUMULATE) {
     if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s);
     return launch_mode<K2_ACCUMULATE, double>(P, s);

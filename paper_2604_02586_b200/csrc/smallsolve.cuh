@@ -422,17 +422,31 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
 #pragma unroll
     for (int j = 0; j < 6; j++) R6[i][j] = 0.0;
   }
+  // eligibility pre-pass (multiview.py:231-235): cheap loads only, so Gaussians with too few
+  // solved views never touch the heavy math
   int n_solved = 0;
   double tw = 0.0;
   int64_t tp = 0;
-  bool bad = false;
   for (int v = 0; v < V; v++) {
     const int64_t gv = (int64_t)v * n + g;
     if (m.status[gv] != TS_STATUS_SOLVED) continue;
     n_solved++;
     tw += m.weight_sum[gv];
     tp += m.pixel_count[gv];
-    if (bad) continue;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    delta[i] = 0.0;
+    sc[i] = gs[7 + i];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) q[i] = gs[3 + i];
+  if (!(n_solved >= cfg.min_views && tw >= cfg.min_total_weight && tp >= cfg.min_total_pixels))
+    return TS_STATUS_UNSOLVABLE;
+  bool bad = false;
+  for (int v = 0; v < V && !bad; v++) {
+    const int64_t gv = (int64_t)v * n + g;
+    if (m.status[gv] != TS_STATUS_SOLVED) continue;
     const ts_camera &cam = cams[v];
     Projection p;
     project(gs, c3, cam, p);
@@ -492,16 +506,7 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     qr_add_row_rhs<6>(R6, c6, L1, mc01);
     qr_add_row_rhs<6>(R6, c6, L2, mc11);
   }
-  const bool eligible = n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
-                        tp >= cfg.min_total_pixels && !bad;
-#pragma unroll
-  for (int i = 0; i < 3; i++) {
-    delta[i] = 0.0;
-    sc[i] = gs[7 + i];
-  }
-#pragma unroll
-  for (int i = 0; i < 4; i++) q[i] = gs[3 + i];
-  if (!eligible) return TS_STATUS_UNSOLVABLE;
+  if (bad) return TS_STATUS_UNSOLVABLE;
   double mean[3], sol[6], qo[4], so[3];
   bool ok = triangulate_from_r(R4, mean);
   ok = ok && cov_from_r(R6, c6, sol);

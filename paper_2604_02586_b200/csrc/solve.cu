@@ -14,63 +14,9 @@
 // ((w*h_i)*h_j, no FMA), so the result equals np.add.at bit-for-bit.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "motion.cuh"
 
 namespace ts {
-
-// Partial-pivot LU solve of a 3x3 system with 2 right-hand sides.  Returns det(A).
-__device__ __forceinline__ double lu3_solve(double A[3][3], double B[3][2]) {
-  double det = 1.0;
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    int piv = k;
-    double best = fabs(A[k][k]);
-#pragma unroll
-    for (int i = k + 1; i < 3; i++)
-      if (fabs(A[i][k]) > best) {
-        best = fabs(A[i][k]);
-        piv = i;
-      }
-    if (piv != k) {
-      det = -det;
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        double t = A[k][j];
-        A[k][j] = A[piv][j];
-        A[piv][j] = t;
-      }
-#pragma unroll
-      for (int j = 0; j < 2; j++) {
-        double t = B[k][j];
-        B[k][j] = B[piv][j];
-        B[piv][j] = t;
-      }
-    }
-    const double d = A[k][k];
-    det *= d;
-    if (d == 0.0) continue;
-#pragma unroll
-    for (int i = k + 1; i < 3; i++) {
-      const double l = A[i][k] / d;
-#pragma unroll
-      for (int j = k + 1; j < 3; j++) A[i][j] -= l * A[k][j];
-#pragma unroll
-      for (int j = 0; j < 2; j++) B[i][j] -= l * B[k][j];
-    }
-  }
-  if (det != 0.0) {
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-#pragma unroll
-      for (int i = 2; i >= 0; i--) {
-        double s = B[i][j];
-#pragma unroll
-        for (int k = i + 1; k < 3; k++) s -= A[i][k] * B[k][j];
-        B[i][j] = s / A[i][i];
-      }
-    }
-  }
-  return det;
-}
 
 __device__ __forceinline__ bool finite6(const double *x) {
   bool ok = true;
@@ -83,59 +29,28 @@ __global__ void __launch_bounds__(256) k3_solve(const Partial *__restrict__ part
                                                 const uint8_t *__restrict__ flag,
                                                 const uint32_t *__restrict__ inst_base,
                                                 const uint32_t *__restrict__ ntiles,
-                                                const RasterRec *__restrict__ rec,
+                                                const int16_t *__restrict__ bbox,
                                                 int64_t NV, double det_floor, int min_pixels,
                                                 double min_weight, ts_motions m) {
   int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gv >= NV) return;
   const uint32_t nt = ntiles[gv];
-  double mom[TS_NMOM];
-#pragma unroll
-  for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
-  uint32_t cnt = 0, scnt = 0;
-  double ax = 0.0, ay = 0.0;
+  GvMotion r;
   if (nt) {
-    // 4 quadrant sub-slots per (tile, Gaussian) instance, added in fixed order
-    const uint32_t base = 4u * inst_base[gv];
-    for (uint32_t i = 0; i < 4u * nt; i++) {
-      if (!flag[base + i]) continue;
-      const Partial &p = partial[base + i];
-#pragma unroll
-      for (int k = 0; k < TS_NMOM; k++) mom[k] += p.m[k];
-      cnt += p.count;
-      scnt += p.static_count;
-    }
-    const RasterRec r = rec[gv];
-    ax = (double)anchor_x(r);
-    ay = (double)anchor_y(r);
+    const short4 bb = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
+    r = solve_gv(partial, flag, 4u * inst_base[gv], 4u * nt, ((int)bb.x + (int)bb.y) >> 1,
+                 ((int)bb.z + (int)bb.w) >> 1, det_floor, min_pixels, min_weight);
+  } else {
+    r = solve_gv(partial, flag, 0, 0, 0, 0, det_floor, min_pixels, min_weight);
   }
-  int8_t status = TS_STATUS_UNSOLVABLE;
-  double A[4] = {1.0, 0.0, 0.0, 1.0}, bvec[2] = {0.0, 0.0};
-  if ((int)cnt >= min_pixels && mom[0] >= min_weight) {
-    double V1[3][3] = {{mom[3], mom[4], mom[1]}, {mom[4], mom[5], mom[2]}, {mom[1], mom[2], mom[0]}};
-    double X[3][2] = {{mom[8], mom[9]}, {mom[10], mom[11]}, {mom[6], mom[7]}};
-    const double det = lu3_solve(V1, X);
-    if (det >= det_floor) {
-      // ab = [A^T; b_a^T] -> A = ab[:2].T, b_a = ab[2]  (motion2d.py:177)
-      double a00 = X[0][0], a01 = X[1][0], a10 = X[0][1], a11 = X[1][1];
-      double b0 = X[2][0] + ax - (a00 * ax + a01 * ay);
-      double b1 = X[2][1] + ay - (a10 * ax + a11 * ay);
-      double res[6] = {a00, a01, a10, a11, b0, b1};
-      if (finite6(res)) {
-        status = TS_STATUS_SOLVED;
-        A[0] = a00; A[1] = a01; A[2] = a10; A[3] = a11;
-        bvec[0] = b0; bvec[1] = b1;
-      }
-    }
-  }
-  m.status[gv] = status;
-  reinterpret_cast<double2 *>(m.a)[2 * gv] = make_double2(A[0], A[1]);
-  reinterpret_cast<double2 *>(m.a)[2 * gv + 1] = make_double2(A[2], A[3]);
-  reinterpret_cast<double2 *>(m.b)[gv] = make_double2(bvec[0], bvec[1]);
-  m.weight_sum[gv] = mom[0];
-  m.pixel_count[gv] = (int32_t)cnt;
-  if (m.static_pixel_count) m.static_pixel_count[gv] = (int32_t)scnt;
-  if (m.static_weight_sum) m.static_weight_sum[gv] = mom[12];
+  m.status[gv] = r.status;
+  reinterpret_cast<double2 *>(m.a)[2 * gv] = make_double2(r.a[0], r.a[1]);
+  reinterpret_cast<double2 *>(m.a)[2 * gv + 1] = make_double2(r.a[2], r.a[3]);
+  reinterpret_cast<double2 *>(m.b)[gv] = make_double2(r.b[0], r.b[1]);
+  m.weight_sum[gv] = r.wsum;
+  m.pixel_count[gv] = (int32_t)r.count;
+  if (m.static_pixel_count) m.static_pixel_count[gv] = (int32_t)r.static_count;
+  if (m.static_weight_sum) m.static_weight_sum[gv] = r.static_wsum;
 }
 
 // solve_view on absolute moments (motion2d.py:164-184).
@@ -232,10 +147,10 @@ __global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ se
 static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
-                     const uint32_t *ntiles, const RasterRec *rec, int64_t nv_total,
+                     const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, cudaStream_t s) {
   if (nv_total)
-    k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, rec, nv_total,
+    k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, bbox, nv_total,
                                                    cfg.det_floor, cfg.min_pixels, cfg.min_weight,
                                                    m);
 }
