@@ -29,6 +29,7 @@ namespace ts {
 constexpr int K2_WARPS = 4;     // warps per CTA (independent; shared memory partitioned)
 constexpr int K2_FLUSH = 8;     // evaluated Gaussians per transposed reduction
 constexpr int K2_WROW = 65;     // padded row of the w buffer (64 pixels)
+constexpr int K2_ETAB_BYTES = ((TS_EXP_TABLE * 8 + 127) / 128) * 128;
 
 struct K2Params {
   const RasterRec *rec;
@@ -58,6 +59,14 @@ struct K2Params {
   // optional work counters (debug; nullptr in production): see K2_STAT_*
   unsigned long long *stats;
 };
+
+// Work counters are compiled in only with -DTS_K2_STATS (they cost ~15 instructions per
+// evaluated Gaussian); tools/profile_frame.py + TS_K2_STATS=1 prints them.
+#ifdef TS_K2_STATS
+#define K2_STATS_ON (P.stats != nullptr)
+#else
+#define K2_STATS_ON false
+#endif
 
 enum { K2S_UNITS, K2S_CHUNKS, K2S_INSTANCES, K2S_HITS, K2S_SKIPS, K2S_EVAL_GAUSS, K2S_EVAL_PIX,
        K2S_CONTRIB, K2S_FLUSHES, K2S_N };
@@ -111,11 +120,12 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
 template <int MODE, typename TrackT>
 __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-  __shared__ double etab[TS_EXP_TABLE];  // exp(-k/64), k = 0..288
+  double *etab = reinterpret_cast<double *>(k2_smem_raw);  // exp(-k/64), k = 0..288
   for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  K2Warp<TrackT> &S = reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw)[warp];
+  K2Warp<TrackT> &S =
+      reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
   const uint32_t n_units = 4u * *P.n_items;
   unsigned long long st[K2S_N] = {};
 
@@ -169,10 +179,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
     // saturated pixels of the quadrant (bit = row * 8 + col), warp-uniform
     uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
                       ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
-    if (P.stats) st[K2S_UNITS]++;
+    if (K2_STATS_ON) st[K2S_UNITS]++;
     for (uint32_t b = start; b < end; b += 32) {
       if (done64 == ~0ull) break;
-      if (P.stats) {
+      if (K2_STATS_ON) {
         st[K2S_CHUNKS]++;
         st[K2S_INSTANCES] += min(32u, end - b);
       }
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
         }
       }
       uint32_t mask = __ballot_sync(0xffffffffu, hit);
-      if (P.stats) st[K2S_HITS] += __popc(mask);
+      if (K2_STATS_ON) st[K2S_HITS] += __popc(mask);
       __syncwarp();
       while (mask) {
         // evaluate up to K2_FLUSH hitting Gaussians in depth order
@@ -211,10 +221,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
           // warp-uniform skip of Gaussians that only cover saturated pixels
           const uint64_t cand = S.rect[j] & ~done64;
           if (cand == 0ull) {
-            if (P.stats) st[K2S_SKIPS]++;
+            if (K2_STATS_ON) st[K2S_SKIPS]++;
             continue;
           }
-          if (P.stats) {
+          if (K2_STATS_ON) {
             st[K2S_EVAL_GAUSS]++;
             st[K2S_EVAL_PIX] += __popcll(cand);
           }
@@ -232,7 +242,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
             if (k1) S.w[k][lane + 32] = w1;
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
             const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
-            if (P.stats) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
+            if (K2_STATS_ON) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
             if ((lane & 7) == k) {
               const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
               my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
         if (MODE == K2_ACCUMULATE) {
           __syncwarp();
           if (__any_sync(0xffffffffu, my_cm != 0)) {
-            if (P.stats) st[K2S_FLUSHES]++;
+            if (K2_STATS_ON) st[K2S_FLUSHES]++;
             // lane: Gaussian kk = lane & 7 of this flush, pixel quarter qq = lane >> 3
             const int kk = lane & 7, qq = lane >> 3;
             double m[TS_NMOM];
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
       }
     }
   }
-  if (P.stats && lane == 0)
+  if (K2_STATS_ON && lane == 0)
     for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);
 }
 
@@ -374,7 +384,7 @@ __global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, 
 template <int MODE, typename TrackT>
 static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
   auto kern = k2_raster<MODE, TrackT>;
-  const size_t smem = sizeof(K2Warp<TrackT>) * K2_WARPS;
+  const size_t smem = K2_ETAB_BYTES + sizeof(K2Warp<TrackT>) * K2_WARPS;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
