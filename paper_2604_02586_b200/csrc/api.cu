@@ -417,8 +417,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!p || !updates || p->V < 1) return TS_E_INVALID_ARGUMENT;
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
   const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
-  ENSURE(p->partial, sizeof(Partial) * 4 * (ni + 1));
-  ENSURE(p->flag, 4 * (ni + 1));
+  ENSURE(p->partial, sizeof(Partial) * TS_K2_SUBS * (ni + 1));
+  ENSURE(p->flag, TS_K2_SUBS * (ni + 1));
   ts_motions m = motions ? *motions : ts_motions{};
   ts_motions im;
   {
@@ -438,7 +438,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   cudaEvent_t e3 = p->mark_begin(s);
-  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, 4 * (ni + 1), s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, TS_K2_SUBS * (ni + 1), s));
   TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
                         ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,

@@ -5,18 +5,14 @@
 //
 // Work decomposition.  K1 bins Gaussians into 16x16-pixel tiles, each tile's list in the
 // reference order (depth, gid).  K2 is a persistent kernel whose WARPS are independent: a warp
-// pulls a work item (tile, 8x8 quadrant) from a global atomic queue and walks the tile list front
-// to back; it stops as soon as all 64 pixels are saturated (T < early_stop) and takes the next
-// item, so occluded Gaussians cost almost nothing.  No block barrier in the main loop.
+// pulls a work item (tile, quadrant) from a global atomic queue, owns that 8x8-pixel quadrant
+// (lane l holds pixels l and l+32, two independent fp64 chains for ILP) and walks the tile list
+// front to back.  No block barrier in the main loop: a warp stops as soon as its 64 pixels are
+// saturated (T < early_stop) and takes the next item, so occluded Gaussians cost almost nothing.
 //   * Culling: per 32-instance chunk, each lane loads one record and computes the 64-bit mask of
-//     quadrant pixels inside its bbox; a ballot keeps the Gaussians whose mask meets an
-//     unsaturated pixel; the candidate mask (bbox AND NOT saturated) is re-checked warp-uniformly
-//     before each Gaussian.
-//   * Compacted evaluation: the per-pixel transmittances live in shared memory, and the candidate
-//     pixels of the current Gaussian are scattered onto consecutive lanes (rank = popcount of
-//     the lower candidate bits), so one pass of the warp evaluates all of them (typically 12 of
-//     the 64 quadrant pixels).  Order per pixel is preserved because Gaussians are processed one
-//     after the other in list order.
+//     quadrant pixels inside its bbox; one ballot keeps the Gaussians whose mask meets an
+//     unsaturated pixel.  Per evaluated Gaussian the candidate mask (bbox AND NOT saturated) is
+//     re-checked warp-uniformly, so Gaussians over saturated pixels cost a few instructions.
 //   * Predicates in fp64 in the reference's operation order (bit-exact q and alpha >= cutoff;
 //     T >= early_stop up to the reference's own log-cumsum rounding).
 //   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp [8 x 64]
@@ -60,11 +56,12 @@ struct K2Params {
   const double *depth64;
   int64_t *dom_gid;
   double *dom_depth;
-  // optional work counters (debug; nullptr in production)
+  // optional work counters (debug; nullptr in production): see K2_STAT_*
   unsigned long long *stats;
 };
 
-// Work counters are compiled in only with -DTS_K2_STATS; TS_K2_STATS=1 at run time prints them.
+// Work counters are compiled in only with -DTS_K2_STATS (they cost ~15 instructions per
+// evaluated Gaussian); tools/profile_frame.py + TS_K2_STATS=1 prints them.
 #ifdef TS_K2_STATS
 #define K2_STATS_ON (P.stats != nullptr)
 #else
@@ -79,17 +76,9 @@ struct K2Warp {
   RasterRec rec[32];
   uint64_t rect[32];  // bbox of the record clipped to the quadrant, as a 64-pixel bit mask
   uint32_t slot[32];
-  double T[64];       // per-pixel transmittance (front-to-back product)
-  union {
-    double w[K2_FLUSH][K2_WROW];  // accumulate mode: w = alpha*T of the current flush group
-    struct {                      // emit / dominant mode per-pixel state
-      double best_w[64];
-      uint32_t seq[64], best_g[64], best_gv[64];
-    };
-  };
+  double w[K2_FLUSH][K2_WROW];
   TrackT trk_u[64], trk_v[64];  // track targets in their input precision
   uint8_t trk_static[64];
-  uint8_t plist[64];  // candidate pixels of the current Gaussian, compacted
 };
 
 // 64-bit mask (bit = row * 8 + col) of the quadrant pixels inside the record's bbox.
@@ -103,10 +92,29 @@ __device__ __forceinline__ uint64_t quad_rect(const RasterRec &r, int qx0, int q
   return (cols * 0x0101010101010101ull) & hi & ~lo;
 }
 
-__device__ __forceinline__ uint64_t warp_or64(uint64_t x) {
-  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)x);
-  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(x >> 32));
-  return ((uint64_t)hi << 32) | lo;
+// One pixel of a lane: predicate evaluation and front-to-back compositing (splat.py:147-193).
+struct PixelState {
+  double T;
+  bool done;
+};
+
+__device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double fpx, double fpy,
+                                           double cutoff, double early_stop, const double *etab,
+                                           PixelState &ps, double &a_out, double &w_out,
+                                           double &tin_out) {
+  if (!cand) return false;  // outside the bbox, or already saturated
+  const double dx = sub(fpx, r.mx), dy = sub(fpy, r.my);
+  const double q = mahalanobis(r, dx, dy);
+  if (!(q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS)) return false;
+  const double a = alpha_of_table(r.opacity, q, etab);
+  if (!(a >= cutoff)) return false;
+  const double tin = ps.T;
+  w_out = mul(a, tin);  // motion2d.py:151
+  ps.T = mul(tin, sub(1.0, a));
+  if (!(ps.T >= early_stop)) ps.done = true;
+  a_out = a;
+  tin_out = tin;
+  return true;
 }
 
 template <int MODE, typename TrackT>
@@ -120,7 +128,6 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
       reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
   const uint32_t n_units = 4u * *P.n_items;
   unsigned long long st[K2S_N] = {};
-  const uint32_t lane_lt = (1u << lane) - 1u;
 
   for (;;) {
     uint32_t unit = 0;
@@ -134,19 +141,20 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
     const int t = tile - v * P.tiles_per_view;
     const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
     const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 8;
-    if (K2_STATS_ON) st[K2S_UNITS]++;
+    // lane pixels: p0 = lane (rows 0-3), p1 = lane + 32 (rows 4-7) of the 8x8 quadrant
+    const int px = qx0 + (lane & 7);
+    const int py0 = qy0 + (lane >> 3), py1 = py0 + 4;
+    const double fpx = (double)px, fpy0 = (double)py0, fpy1 = (double)py1;
+    const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
 
-    // per-pixel state for pixels p = lane and p = lane + 32 (bit p = row * 8 + col)
-    uint64_t valid64 = 0, done64 = 0;
+    bool valid0 = false, valid1 = false;
+    if (MODE == K2_ACCUMULATE) {
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int p = lane + 32 * h;
-      const int px = qx0 + (p & 7), py = qy0 + (p >> 3);
-      const bool in = px < P.W && py < P.H;
-      bool val = false;
-      if (MODE == K2_ACCUMULATE) {
+      for (int h = 0; h < 2; h++) {
+        const int py = h ? py1 : py0;
         TrackT u = TrackT(0), vv = TrackT(0);
-        if (in) {
+        bool val = false;
+        if (h ? in1 : in0) {
           const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
           val = P.track_valid[pix] != 0;
           if (val) {
@@ -155,22 +163,23 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
             vv = __ldg(tg + 1);
           }
         }
+        const int p = lane + 32 * h;
         S.trk_u[p] = u;
         S.trk_v[p] = vv;
         S.trk_static[p] = val && is_static((double)u, (double)vv, px, py, P.static_thr);
-      } else if (MODE == K2_EMIT) {
-        S.seq[p] = 0;
-      } else {
-        S.best_w[p] = -1.0;
-        S.best_g[p] = 0xFFFFFFFFu;
+        if (h) valid1 = val; else valid0 = val;
       }
-      S.T[p] = 1.0;
-      const uint64_t vb = (uint64_t)__ballot_sync(0xffffffffu, val);
-      const uint64_t db = (uint64_t)__ballot_sync(0xffffffffu, !in || !(1.0 >= P.early_stop));
-      valid64 |= vb << (32 * h);
-      done64 |= db << (32 * h);
     }
+    PixelState s0{1.0, !in0 || !(1.0 >= P.early_stop)};
+    PixelState s1{1.0, !in1 || !(1.0 >= P.early_stop)};
+    uint32_t seq0 = 0, seq1 = 0;                  // emit mode
+    double best_w0 = -1.0, best_w1 = -1.0;        // dominant mode
+    uint32_t best_g0 = 0xFFFFFFFFu, best_g1 = 0xFFFFFFFFu, best_gv0 = 0, best_gv1 = 0;
 
+    // saturated pixels of the quadrant (bit = row * 8 + col), warp-uniform
+    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
+                      ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
+    if (K2_STATS_ON) st[K2S_UNITS]++;
     for (uint32_t b = start; b < end; b += 32) {
       if (done64 == ~0ull) break;
       if (K2_STATS_ON) {
@@ -215,70 +224,63 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
             if (K2_STATS_ON) st[K2S_SKIPS]++;
             continue;
           }
-          const uint32_t clo = (uint32_t)cand, chi = (uint32_t)(cand >> 32);
-          const int nlo = __popc(clo), n = nlo + __popc(chi);
           if (K2_STATS_ON) {
             st[K2S_EVAL_GAUSS]++;
-            st[K2S_EVAL_PIX] += n;
+            st[K2S_EVAL_PIX] += __popcll(cand);
           }
-          // compact the candidate pixels onto lanes 0..n-1 (rank = popcount of lower bits)
-          if ((clo >> lane) & 1u) S.plist[__popc(clo & lane_lt)] = (uint8_t)lane;
-          if ((chi >> lane) & 1u) S.plist[nlo + __popc(chi & lane_lt)] = (uint8_t)(lane + 32);
-          __syncwarp();
-          const RasterRec &r = S.rec[j];
-          uint64_t newly_done = 0, contrib = 0;
-          for (int base = 0; base < n; base += 32) {
-            const int l = base + lane;
-            if (l < n) {
-              const int p = S.plist[l];
-              const double dx = sub((double)(qx0 + (p & 7)), r.mx);
-              const double dy = sub((double)(qy0 + (p >> 3)), r.my);
-              const double q = mahalanobis(r, dx, dy);
-              if (q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS) {
-                const double a = alpha_of_table(r.opacity, q, etab);
-                if (a >= P.alpha_cutoff) {
-                  const double tin = S.T[p];
-                  const double w = mul(a, tin);  // motion2d.py:151
-                  const double tn = mul(tin, sub(1.0, a));
-                  S.T[p] = tn;
-                  if (!(tn >= P.early_stop)) newly_done |= 1ull << p;
-                  if (MODE == K2_ACCUMULATE) {
-                    if ((valid64 >> p) & 1ull) {
-                      S.w[k][p] = w;
-                      contrib |= 1ull << p;
-                    }
-                  } else if (MODE == K2_EMIT) {
-                    const unsigned long long o = atomicAdd(P.emit_count, 1ull);
-                    if ((int64_t)o < P.emit_cap) {
-                      const int px = qx0 + (p & 7), py = qy0 + (p >> 3);
-                      P.emit_key[o] = ((uint64_t)((uint32_t)(py * P.W + px)) << 32) | S.seq[p];
-                      P.emit_gv[o] = S.slot[j];
-                      P.emit_alpha[o] = a;
-                      P.emit_trans[o] = tin;
-                    }
-                    S.seq[p]++;
-                  } else {  // K2_DOMINANT: argmax alpha*T, ties by smaller id (scene.py:179)
-                    const uint32_t g = r.g;
-                    if (w > S.best_w[p] || (w == S.best_w[p] && g < S.best_g[p])) {
-                      S.best_w[p] = w;
-                      S.best_g[p] = g;
-                      S.best_gv[p] = S.slot[j];
-                    }
-                  }
-                }
-              }
-            }
-          }
-          done64 |= warp_or64(newly_done);
+          const RasterRec r = S.rec[j];
+          double a0 = 0, w0 = 0, t0 = 0, a1 = 0, w1 = 0, t1 = 0;
+          const bool c0 = eval_pixel(r, (cand >> lane) & 1ull, fpx, fpy0, P.alpha_cutoff,
+                                     P.early_stop, etab, s0, a0, w0, t0);
+          const bool c1 = eval_pixel(r, (cand >> (lane + 32)) & 1ull, fpx, fpy1, P.alpha_cutoff,
+                                     P.early_stop, etab, s1, a1, w1, t1);
+          done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
+                   ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
           if (MODE == K2_ACCUMULATE) {
-            const uint64_t cm = warp_or64(contrib);
-            if (K2_STATS_ON) st[K2S_CONTRIB] += __popcll(cm);
+            const bool k0 = c0 && valid0, k1 = c1 && valid1;
+            if (k0) S.w[k][lane] = w0;
+            if (k1) S.w[k][lane + 32] = w1;
+            const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
+            const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
+            if (K2_STATS_ON) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
             if ((lane & 7) == k) {
-              my_cm = (uint32_t)(cm >> (16 * (lane >> 3))) & 0xFFFFu;
+              const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
+              my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
               my_j = j;
             }
+          } else if (MODE == K2_EMIT) {
+            if (c0 || c1) {
+              const unsigned long long idx = atomicAdd(P.emit_count, (unsigned long long)(c0 + c1));
+              unsigned long long o = idx;
+              if (c0 && (int64_t)o < P.emit_cap) {
+                P.emit_key[o] = ((uint64_t)((uint32_t)(py0 * P.W + px)) << 32) | seq0;
+                P.emit_gv[o] = S.slot[j];
+                P.emit_alpha[o] = a0;
+                P.emit_trans[o] = t0;
+              }
+              if (c0) o++;
+              if (c1 && (int64_t)o < P.emit_cap) {
+                P.emit_key[o] = ((uint64_t)((uint32_t)(py1 * P.W + px)) << 32) | seq1;
+                P.emit_gv[o] = S.slot[j];
+                P.emit_alpha[o] = a1;
+                P.emit_trans[o] = t1;
+              }
+            }
+            seq0 += c0;
+            seq1 += c1;
+          } else {  // K2_DOMINANT: argmax alpha*T, ties by smaller id (scene.py:179)
+            const uint32_t g = r.g;
+            if (c0 && (w0 > best_w0 || (w0 == best_w0 && g < best_g0))) {
+              best_w0 = w0;
+              best_g0 = g;
+              best_gv0 = S.slot[j];
+            }
+            if (c1 && (w1 > best_w1 || (w1 == best_w1 && g < best_g1))) {
+              best_w1 = w1;
+              best_g1 = g;
+              best_gv1 = S.slot[j];
+            }
           }
-          __syncwarp();
           k++;
         }
         if (MODE == K2_ACCUMULATE) {
@@ -349,20 +351,17 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
       }
     }
     if (MODE == K2_DOMINANT) {
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int p = lane + 32 * h;
-        const int px = qx0 + (p & 7), py = qy0 + (p >> 3);
-        if (px < P.W && py < P.H) {
-          const int64_t pix = (int64_t)py * P.W + px;
-          const uint32_t g = S.best_g[p];
-          P.dom_gid[pix] = g != 0xFFFFFFFFu ? (int64_t)g : -1;
-          P.dom_depth[pix] = g != 0xFFFFFFFFu ? P.depth64[S.best_gv[p]] : 0.0;
-        }
+      if (in0) {
+        const int64_t pix = (int64_t)py0 * P.W + px;
+        P.dom_gid[pix] = best_g0 != 0xFFFFFFFFu ? (int64_t)best_g0 : -1;
+        P.dom_depth[pix] = best_g0 != 0xFFFFFFFFu ? P.depth64[best_gv0] : 0.0;
+      }
+      if (in1) {
+        const int64_t pix = (int64_t)py1 * P.W + px;
+        P.dom_gid[pix] = best_g1 != 0xFFFFFFFFu ? (int64_t)best_g1 : -1;
+        P.dom_depth[pix] = best_g1 != 0xFFFFFFFFu ? P.depth64[best_gv1] : 0.0;
       }
     }
-    __syncwarp();
   }
   if (K2_STATS_ON && lane == 0)
     for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) k3_solve(const Partial *__restrict__ part
   GvMotion r;
   if (nt) {
     const short4 bb = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
-    r = solve_gv(partial, flag, 4u * inst_base[gv], 4u * nt, ((int)bb.x + (int)bb.y) >> 1,
+    r = solve_gv(partial, flag, TS_K2_SUBS * inst_base[gv], TS_K2_SUBS * nt, ((int)bb.x + (int)bb.y) >> 1,
                  ((int)bb.z + (int)bb.w) >> 1, det_floor, min_pixels, min_weight);
   } else {
     r = solve_gv(partial, flag, 0, 0, 0, 0, det_floor, min_pixels, min_weight);
