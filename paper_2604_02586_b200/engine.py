@@ -174,3 +174,69 @@ class FrameEngine:
                                                   nat.dptr(dep), nat.stream_ptr(stream)),
                   "ts_dominant_gaussians")
         return gid, dep
+
+
+class StreamingEngine:
+    """Double-buffered end-to-end driver: pinned host inputs in, pinned host results out.
+
+    Every step copies its own inputs (Gaussians + tracks) host->device and reads its result back
+    device->host; the copies of step k+1 run on a copy stream while step k computes on the
+    compute stream (two input slots, ordered with CUDA events).  This is how a caller streams the
+    target frames of a clip through the hot path.
+    """
+
+    def __init__(self, engine: FrameEngine | None = None):
+        torch = _torch()
+        self.eng = engine if engine is not None else FrameEngine()
+        self.copy_stream = torch.cuda.Stream()
+        self.comp_stream = torch.cuda.Stream()
+        self._slots = [None, None]
+        self._free = [None, None]
+        self._k = 0
+        self.out = None
+
+    def _slot(self, i, g_host, t_host, v_host):
+        torch = _torch()
+        s = self._slots[i]
+        shapes = (tuple(g_host.shape), tuple(t_host.shape), tuple(v_host.shape), t_host.dtype)
+        if s is None or s[0] != shapes:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            s = (shapes, torch.empty(g_host.shape, dtype=torch.float64, device=dev),
+                 torch.empty(t_host.shape, dtype=t_host.dtype, device=dev),
+                 torch.empty(v_host.shape, dtype=torch.uint8, device=dev))
+            self._slots[i] = s
+        return s[1], s[2], s[3]
+
+    @staticmethod
+    def result_buffer(n):
+        """Pinned host buffer for one step's result rows: delta(3) rotation(4) scale(3) status."""
+        torch = _torch()
+        return torch.empty((n, 11), dtype=torch.float64).pin_memory()
+
+    def step(self, g_host, cameras, t_host, v_host, res_host, config=None):
+        """Enqueue one frame: H2D inputs, K1..K4, D2H result.  Returns the completion event."""
+        torch = _torch()
+        i = self._k % 2
+        self._k += 1
+        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host)
+        with torch.cuda.stream(self.copy_stream):
+            if self._free[i] is not None:
+                self.copy_stream.wait_event(self._free[i])
+            g_d.copy_(g_host, non_blocking=True)
+            t_d.copy_(t_host, non_blocking=True)
+            v_d.copy_(v_host, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self.copy_stream)
+        cs = self.comp_stream
+        cs.wait_event(ready)
+        self.eng.bin(g_d, cameras, config, stream=cs)
+        self.out = self.eng.compensate(t_d, v_d, self.out, stream=cs)
+        with torch.cuda.stream(cs):
+            o = self.out
+            res = torch.cat([o.delta_mean, o.rotation, o.scale,
+                             o.status.to(torch.float64)[:, None]], 1)
+            res_host.copy_(res, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+        self._free[i] = done
+        return done
