@@ -185,6 +185,56 @@ int ts_decompose_batch(const double *sigma, const double *ref_quat, int64_t batc
 int ts_dominant_gaussians(ts_plan *plan, int32_t view, int64_t *gid_img, double *depth_img,
                           void *stream);
 
+/* ---- Regularisation (regularize.py:37-188; glue pipeline.py:88-98) ------------------------- *
+ * Frame-1 Gaussians are (N, 11) rows as in ts_frame_bin; update arrays as ts_updates; per-view
+ * counts in the (V*N) view-major layout of ts_motions.  Adjacency is (N, kk) int64, kk =
+ * min(k, N-1) <= TS_KNN_MAX_K, rows sorted by (distance, id) ascending. */
+#define TS_KNN_MAX_K 32
+#define TS_AVERAGE_MEAN 0
+#define TS_AVERAGE_MEDIAN 1
+
+typedef struct ts_reg_config { /* Config fields used by _fuse_frame (pipeline.py:88-96) */
+  int32_t min_hit_pixels;  /* 9   */
+  int32_t min_views;       /* 2   */
+  double static_fraction;  /* 0.9 */
+  int32_t average;         /* TS_AVERAGE_MEAN / TS_AVERAGE_MEDIAN (propagation_average) */
+  int32_t reserved;
+} ts_reg_config;
+
+/* build_knn (regularize.py:37-53): exact k nearest neighbours of each point by Euclidean
+ * distance, ties by smaller id.  positions: n points of 3 doubles, `row_stride` doubles apart
+ * (3 for an (N,3) array, 11 to read the means of Gaussian rows).  Uses the plan's workspace.
+ * TS_E_INVALID_ARGUMENT for n < 2, k < 1 or min(k, n-1) > TS_KNN_MAX_K. */
+int ts_build_knn(ts_plan *plan, const double *positions, int64_t row_stride, int64_t n, int32_t k,
+                 int64_t *adjacency, void *stream);
+
+/* detect_static_all (regularize.py:77-88) on view-major (V*N) counts -> flags (N) uint8. */
+int ts_detect_static(const int32_t *pixel_count, const int32_t *static_pixel_count, int64_t n,
+                     int32_t n_views, const ts_reg_config *config, uint8_t *static_flags,
+                     void *stream);
+
+/* median_filter (regularize.py:91-121): `out` must not alias `in`. */
+int ts_median_filter(const double *frame1, int64_t n, const ts_updates *in,
+                     const int64_t *adjacency, int32_t kk, const ts_updates *out, void *stream);
+
+/* propagate (regularize.py:124-174) with given static flags; `out` must not alias `in`. */
+int ts_propagate(ts_plan *plan, const double *frame1, int64_t n, const ts_updates *in,
+                 const int64_t *adjacency, int32_t kk, const uint8_t *static_flags,
+                 int32_t average, const ts_updates *out, void *stream);
+
+/* apply_updates (regularize.py:177-188) -> (N, 11) rows. */
+int ts_apply_updates(const double *frame1, int64_t n, const ts_updates *updates, double *rows_out,
+                     void *stream);
+
+/* The regularisation tail of _fuse_frame (pipeline.py:88-98) in two kernels: static flags from
+ * the K2 counts, median filter, propagation and apply_updates.  `in` is the ts_update_all /
+ * ts_frame_compensate output; `out` (must not alias `in`) receives the final updates,
+ * `static_flags` (nullable) the flags and `rows_out` (nullable) the updated Gaussians. */
+int ts_regularize(ts_plan *plan, const double *frame1, int64_t n, const ts_updates *in,
+                  const int32_t *pixel_count, const int32_t *static_pixel_count, int32_t n_views,
+                  const int64_t *adjacency, int32_t kk, const ts_reg_config *config,
+                  const ts_updates *out, uint8_t *static_flags, double *rows_out, void *stream);
+
 /* Synchronous device -> host copy (lets ctypes/cgo/JNI bindings read plan-owned arrays). */
 int ts_memcpy_d2h(void *host_dst, const void *device_src, int64_t bytes);
 

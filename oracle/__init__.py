@@ -64,6 +64,10 @@ def _lib():
         lib.orc_accumulate.argtypes = [i64, ptr, ptr, ptr, ptr, ptr, ctypes.c_int, ctypes.c_int,
                                        ptr, ptr, i64, dbl, ptr, ptr, ptr, ptr, ptr, ptr]
         lib.orc_accumulate.restype = None
+        lib.orc_knn.argtypes = [i64, ptr, ctypes.c_int, ptr]
+        lib.orc_knn.restype = None
+        lib.orc_knn_queries.argtypes = [i64, ptr, ctypes.c_int, i64, ptr, ptr]
+        lib.orc_knn_queries.restype = None
         _LIB = lib
     return _LIB
 

@@ -311,3 +311,39 @@ void orc_accumulate(int64_t m, const int32_t *px, const int32_t *py, const int64
     }
   }
 }
+
+/* build_knn (regularize.py:37-53): brute force over all pairs; distance exactly as
+ * np.linalg.norm(positions - positions[i], axis=1) = sqrt((dx*dx + dy*dy) + dz*dz),
+ * dx = p_j - p_i; the kk best by (distance, id) in ascending order. */
+void orc_knn_queries(int64_t n, const double *pos, int kk, int64_t nq, const int64_t *qidx,
+                     int64_t *adj) {
+  double *bd = (double *)malloc(sizeof(double) * (size_t)(kk + 1));
+  int64_t *bi = (int64_t *)malloc(sizeof(int64_t) * (size_t)(kk + 1));
+  for (int64_t r = 0; r < nq; r++) {
+    const int64_t i = qidx ? qidx[r] : r;
+    int cnt = 0;
+    const double *q = pos + 3 * i;
+    for (int64_t j = 0; j < n; j++) {
+      if (j == i) continue;
+      const double *p = pos + 3 * j;
+      const double dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
+      const double d = sqrt((dx * dx + dy * dy) + dz * dz);
+      if (cnt == kk && !(d < bd[kk - 1] || (d == bd[kk - 1] && j < bi[kk - 1]))) continue;
+      int s = cnt < kk ? cnt++ : kk - 1;
+      while (s > 0 && (d < bd[s - 1] || (d == bd[s - 1] && j < bi[s - 1]))) {
+        bd[s] = bd[s - 1];
+        bi[s] = bi[s - 1];
+        s--;
+      }
+      bd[s] = d;
+      bi[s] = j;
+    }
+    for (int s = 0; s < kk; s++) adj[r * kk + s] = bi[s];
+  }
+  free(bd);
+  free(bi);
+}
+
+void orc_knn(int64_t n, const double *pos, int kk, int64_t *adj) {
+  orc_knn_queries(n, pos, kk, n, NULL, adj);
+}

@@ -73,6 +73,15 @@ class Binning(ctypes.Structure):
                 ("inst_gv", _vp), ("tile_range", _vp), ("gv_status", _vp), ("gv_bbox", _vp)]
 
 
+class RegConfig(ctypes.Structure):
+    _fields_ = [("min_hit_pixels", ctypes.c_int32), ("min_views", ctypes.c_int32),
+                ("static_fraction", ctypes.c_double), ("average", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+TS_KNN_MAX_K = 32
+_UP = ctypes.POINTER(Updates)
+
 _SIGS = {
     "ts_version": ([], ctypes.c_int),
     "ts_error_string": ([ctypes.c_int], ctypes.c_char_p),
@@ -107,6 +116,17 @@ _SIGS = {
     "ts_decompose_batch": ([_vp, _vp, ctypes.c_int64, ctypes.c_double, _vp, _vp, _vp, _vp],
                            ctypes.c_int),
     "ts_dominant_gaussians": ([_vp, ctypes.c_int32, _vp, _vp, _vp], ctypes.c_int),
+    "ts_build_knn": ([_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp, _vp],
+                     ctypes.c_int),
+    "ts_detect_static": ([_vp, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(RegConfig),
+                          _vp, _vp], ctypes.c_int),
+    "ts_median_filter": ([_vp, ctypes.c_int64, _UP, _vp, ctypes.c_int32, _UP, _vp], ctypes.c_int),
+    "ts_propagate": ([_vp, _vp, ctypes.c_int64, _UP, _vp, ctypes.c_int32, _vp, ctypes.c_int32,
+                      _UP, _vp], ctypes.c_int),
+    "ts_apply_updates": ([_vp, ctypes.c_int64, _UP, _vp, _vp], ctypes.c_int),
+    "ts_regularize": ([_vp, _vp, ctypes.c_int64, _UP, _vp, _vp, ctypes.c_int32, _vp,
+                       ctypes.c_int32, ctypes.POINTER(RegConfig), _UP, _vp, _vp, _vp],
+                      ctypes.c_int),
     "ts_memcpy_d2h": ([_vp, _vp, ctypes.c_int64], ctypes.c_int),
 }
 
@@ -193,6 +213,20 @@ def make_cameras(cams):
     for i, c in enumerate(cams):
         arr[i] = make_camera(c)
     return arr
+
+
+def make_reg_config(cfg=None, average=None) -> RegConfig:
+    """ts_reg_config from a Config (pipeline.py:88-96 fields)."""
+    c = RegConfig()
+    get = (lambda k, d: getattr(cfg, k, d)) if cfg is not None else (lambda k, d: d)
+    c.min_hit_pixels = int(get("min_hit_pixels", 9))
+    c.min_views = int(get("min_views", 2))
+    c.static_fraction = float(get("static_fraction", 0.9))
+    avg = average if average is not None else get("propagation_average", "mean")
+    if avg not in ("mean", "median"):
+        raise ValueError(f"average must be 'mean' or 'median', got {avg}")
+    c.average = 0 if avg == "mean" else 1
+    return c
 
 
 def make_config(cfg=None, early_stop=1e-4) -> Config:

@@ -64,6 +64,9 @@ struct ts_plan {
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
+  // regularisation buffers
+  DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
+      reg_static, reg_source, reg_euler;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
   int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
@@ -114,7 +117,10 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->emit_count, &p->emit_key, &p->emit_key2, &p->emit_gv,
                           &p->emit_alpha, &p->emit_trans, &p->emit_idx, &p->emit_idx2,
                           &p->deg_flags, &p->deg_ids, &p->deg_count, &p->acc_keys, &p->acc_keys2,
-                          &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end};
+                          &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end,
+                          &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
+                          &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
+                          &p->reg_source, &p->reg_euler};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -129,7 +135,9 @@ void release_all(ts_plan *p) {
                     &p->emit_key, &p->emit_key2, &p->emit_gv, &p->emit_alpha, &p->emit_trans,
                     &p->emit_idx, &p->emit_idx2, &p->deg_flags, &p->deg_ids, &p->deg_count,
                     &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
-                    &p->seg_end};
+                    &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
+                    &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
+                    &p->reg_static, &p->reg_source, &p->reg_euler};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -689,7 +697,133 @@ int ts_dominant_gaussians(ts_plan *p, int32_t view, int64_t *gid_img, double *de
   return TS_OK;
 }
 
+// ---- regularisation -------------------------------------------------------------------------
+
+int ts_build_knn(ts_plan *p, const double *positions, int64_t row_stride, int64_t n, int32_t k,
+                 int64_t *adjacency, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || !positions || !adjacency || n < 2 || k < 1 || row_stride < 3 || n >= (1ll << 31))
+    return TS_E_INVALID_ARGUMENT;
+  const int kk = (int)std::min<int64_t>(k, n - 1);
+  if (kk > TS_KNN_MAX_K) return TS_E_INVALID_ARGUMENT;
+  const int64_t cap = 2 * n + 64;  // cell budget (the grid targets ~n/2 cells)
+  const int nb = knn_bound_blocks(n);
+  ENSURE(p->knn_part, 6 * sizeof(double) * nb);
+  ENSURE(p->knn_grid, sizeof(KnnGrid));
+  ENSURE(p->knn_key, 4 * n);
+  ENSURE(p->knn_key2, 4 * n);
+  ENSURE(p->knn_val, 4 * n);
+  ENSURE(p->knn_val2, 4 * n);
+  ENSURE(p->knn_sp, sizeof(double4) * n);
+  ENSURE(p->knn_lo, 4 * cap);
+  ENSURE(p->knn_hi, 4 * cap);
+  TS_CUDA_TRY(cudaMemsetAsync(p->knn_lo.p, 0, 4 * cap, s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->knn_hi.p, 0, 4 * cap, s));
+  KnnGrid *g = ptr<KnnGrid>(p->knn_grid);
+  launch_knn_grid(positions, row_stride, n, cap, ptr<double>(p->knn_part), g,
+                  ptr<uint32_t>(p->knn_key), ptr<uint32_t>(p->knn_val), s);
+  const int bits = bits_for((uint64_t)cap);
+  TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+    return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint32_t>(p->knn_key),
+                                           ptr<uint32_t>(p->knn_key2), ptr<uint32_t>(p->knn_val),
+                                           ptr<uint32_t>(p->knn_val2), (int)n, 0, bits, s);
+  }));
+  launch_knn_gather(positions, row_stride, ptr<uint32_t>(p->knn_key2), ptr<uint32_t>(p->knn_val2),
+                    n, ptr<double4>(p->knn_sp), ptr<uint32_t>(p->knn_lo), ptr<uint32_t>(p->knn_hi),
+                    s);
+  TS_CUDA_TRY(launch_knn_query(kk, ptr<double4>(p->knn_sp), ptr<uint32_t>(p->knn_lo),
+                               ptr<uint32_t>(p->knn_hi), g, n, adjacency, s));
+  return TS_OK;
+}
+
+int ts_detect_static(const int32_t *pixel_count, const int32_t *static_pixel_count, int64_t n,
+                     int32_t n_views, const ts_reg_config *c, uint8_t *static_flags,
+                     void *stream) {
+  if (!pixel_count || !static_pixel_count || !c || !static_flags || n < 0 || n_views < 0)
+    return TS_E_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  launch_static_flags(pixel_count, static_pixel_count, n, n_views, c->min_hit_pixels,
+                      c->static_fraction, c->min_views, static_flags, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+static bool updates_ok(const ts_updates *u) {
+  return u && u->delta_mean && u->rotation && u->scale && u->status;
+}
+
+int ts_median_filter(const double *frame1, int64_t n, const ts_updates *in,
+                     const int64_t *adjacency, int32_t kk, const ts_updates *out, void *stream) {
+  if (!frame1 || !updates_ok(in) || !updates_ok(out) || n < 0 || kk < 0 || kk > TS_KNN_MAX_K ||
+      (n > 0 && kk > 0 && !adjacency))
+    return TS_E_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  launch_reg_filter(REG_MEDIAN_ONLY, frame1, n, *in, nullptr, nullptr, 0, adjacency, kk, 0, 0.0, 0,
+                    *out, nullptr, nullptr, nullptr, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_propagate(ts_plan *p, const double *frame1, int64_t n, const ts_updates *in,
+                 const int64_t *adjacency, int32_t kk, const uint8_t *static_flags,
+                 int32_t average, const ts_updates *out, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || !frame1 || !updates_ok(in) || !updates_ok(out) || !static_flags || n < 0 || kk < 0 ||
+      kk > TS_KNN_MAX_K || (average != TS_AVERAGE_MEAN && average != TS_AVERAGE_MEDIAN) ||
+      (n > 0 && kk > 0 && !adjacency))
+    return TS_E_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  ENSURE(p->reg_source, n);
+  ENSURE(p->reg_euler, 24 * n);
+  launch_reg_filter(REG_PREP_GIVEN_STATIC, frame1, n, *in, nullptr, nullptr, 0, adjacency, kk, 0,
+                    0.0, 0, *out, const_cast<uint8_t *>(static_flags), ptr<uint8_t>(p->reg_source),
+                    ptr<double>(p->reg_euler), s);
+  launch_reg_propagate(true, false, frame1, n, *out, static_flags, ptr<uint8_t>(p->reg_source),
+                       ptr<double>(p->reg_euler), adjacency, kk, average, nullptr, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_apply_updates(const double *frame1, int64_t n, const ts_updates *u, double *rows_out,
+                     void *stream) {
+  if (!frame1 || !updates_ok(u) || !rows_out || n < 0) return TS_E_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  launch_reg_propagate(false, true, frame1, n, *u, nullptr, nullptr, nullptr, nullptr, 0, 0,
+                       rows_out, (cudaStream_t)stream);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_regularize(ts_plan *p, const double *frame1, int64_t n, const ts_updates *in,
+                  const int32_t *pixel_count, const int32_t *static_pixel_count, int32_t n_views,
+                  const int64_t *adjacency, int32_t kk, const ts_reg_config *c,
+                  const ts_updates *out, uint8_t *static_flags, double *rows_out, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p || !frame1 || !updates_ok(in) || !updates_ok(out) || !pixel_count ||
+      !static_pixel_count || !c || n < 0 || n_views < 0 || kk < 0 || kk > TS_KNN_MAX_K ||
+      (c->average != TS_AVERAGE_MEAN && c->average != TS_AVERAGE_MEDIAN) ||
+      (n > 0 && kk > 0 && !adjacency))
+    return TS_E_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  uint8_t *flags = static_flags;
+  if (!flags) {
+    ENSURE(p->reg_static, n);
+    flags = ptr<uint8_t>(p->reg_static);
+  }
+  ENSURE(p->reg_source, n);
+  ENSURE(p->reg_euler, 24 * n);
+  launch_reg_filter(REG_FULL, frame1, n, *in, pixel_count, static_pixel_count, n_views, adjacency,
+                    kk, c->min_hit_pixels, c->static_fraction, c->min_views, *out, flags,
+                    ptr<uint8_t>(p->reg_source), ptr<double>(p->reg_euler), s);
+  launch_reg_propagate(true, rows_out != nullptr, frame1, n, *out, flags,
+                       ptr<uint8_t>(p->reg_source), ptr<double>(p->reg_euler), adjacency, kk,
+                       c->average, rows_out, s);
+  TS_CUDA_TRY(cudaGetLastError());
+  return TS_OK;
+}
+
 }  // extern "C"
+
 
 extern "C" int ts_memcpy_d2h(void *host_dst, const void *device_src, int64_t bytes) {
   if (bytes < 0) return TS_E_INVALID_ARGUMENT;

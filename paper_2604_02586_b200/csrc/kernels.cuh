@@ -61,4 +61,32 @@ void launch_decompose_batch(const double *sigma, const double *ref_quat, int64_t
                             double eig_floor, double *quat, double *scale, int8_t *status,
                             cudaStream_t s);
 
+// Regularisation (regularize.cu)
+#define TS_KNN_MAX_K 32
+struct KnnGrid {
+  double lo[3];
+  double h, inv_h, slack;
+  int dim[3];
+  int ncell;
+};
+enum { REG_MEDIAN_ONLY = 0, REG_PREP_GIVEN_STATIC = 1, REG_FULL = 2 };
+int knn_bound_blocks(int64_t n);
+void launch_knn_grid(const double *pos, int64_t stride, int64_t n, int64_t cap, double *part,
+                     KnnGrid *g, uint32_t *key, uint32_t *val, cudaStream_t s);
+void launch_knn_gather(const double *pos, int64_t stride, const uint32_t *key, const uint32_t *val,
+                       int64_t n, double4 *sp, uint32_t *cell_lo, uint32_t *cell_hi,
+                       cudaStream_t s);
+cudaError_t launch_knn_query(int k, const double4 *sp, const uint32_t *lo, const uint32_t *hi,
+                             const KnnGrid *g, int64_t n, int64_t *adj, cudaStream_t s);
+void launch_static_flags(const int32_t *pix, const int32_t *spix, int64_t n, int V, int min_hit,
+                         double frac, int min_views, uint8_t *flag, cudaStream_t s);
+void launch_reg_filter(int mode, const double *G, int64_t n, ts_updates in, const int32_t *pix,
+                       const int32_t *spix, int V, const int64_t *adj, int kk, int min_hit,
+                       double frac, int min_views, ts_updates out, uint8_t *static_flag,
+                       uint8_t *source_flag, double *rel_euler, cudaStream_t s);
+void launch_reg_propagate(bool propagate, bool apply, const double *G, int64_t n, ts_updates u,
+                          const uint8_t *static_flag, const uint8_t *source_flag,
+                          const double *rel_euler, const int64_t *adj, int kk, int average,
+                          double *rows_out, cudaStream_t s);
+
 }  // namespace ts

@@ -2,10 +2,13 @@
 
 `compensate_frame` keeps the reference signature.  Its four hot-path stages (rasterize,
 accumulate, per-view solve, multi-view fuse: pipeline.py:117-124 and :79-86) run as
-K1 -> K2 -> K3 -> K4 on the device without materialising weight maps or per-view objects.
-The reference's regularisation (kNN median filter, static pinning, propagation,
-regularize.py:37-188) is outside this build's scope; pass `regularize=` to plug it
-in (e.g. `gausstrack_regularizer()` when the reference package is importable).
+K1 -> K2 -> K3 -> K4 on the device without materialising weight maps or per-view objects, and
+the regularisation tail (static flags, kNN median filter, propagation, apply_updates:
+pipeline.py:88-98, regularize.py:37-188) runs as two more kernels on the K4 outputs
+(regularize.regularize_device), with the exact kNN built on the device when `knn` is None.
+`regularize=False` returns the K4 updates unregularised; a callable
+`regularize(frame1, updates, accs, config, knn) -> updates` replaces the stage (e.g.
+`gausstrack_regularizer()`, the reference's CPU implementation, for cross-checks).
 """
 
 from __future__ import annotations
@@ -115,14 +118,35 @@ def _engine():
     return _ENGINES[dev]
 
 
-def compensate_frame(frame1, cameras, tracks, config: Config = None, weightmaps=None, knn=None,
-                     frame_index=0, first_frame_index=0, regularize=None) -> FrameResult:
-    """Single-frame motion compensation from first-frame Gaussians and per-view tracks.
+def _knn_adjacency(knn, rows_dev, config):
+    import torch
 
-    Without `weightmaps` this is the fused GPU path; with them it runs the GPU stage kernels on
-    the given weight maps (as the reference skips its rasterizer).  `regularize(frame1, updates,
-    accs, config, knn) -> updates` optionally applies a regularisation stage.
+    from .regularize import knn_device
+    if knn is None:
+        return knn_device(rows_dev, config.knn_k)
+    adj = np.asarray(knn.adjacency if hasattr(knn, "adjacency") else knn, np.int64)
+    return torch.from_numpy(adj.reshape(len(adj), -1)).to(rows_dev.device)
+
+
+def _result(frame_index, first_frame_index, new_rows, status, t0):
+    st = np.asarray(status)
+    tallies = {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
+               "unsolvable": int((st == 0).sum())}
+    return FrameResult(frame_index, GaussianList(new_rows), tallies,
+                       {"tracking": 0.0, "compensation": time.perf_counter() - t0,
+                        "refinement": 0.0}, compensated_from=first_frame_index)
+
+
+def compensate_frame(frame1, cameras, tracks, config: Config = None, weightmaps=None, knn=None,
+                     frame_index=0, first_frame_index=0, regularize=True) -> FrameResult:
+    """Full single-frame motion compensation from first-frame Gaussians and per-view tracks.
+
+    Without `weightmaps` this is the fused GPU path (K1-K4 + regularisation); with them it runs
+    the GPU stage kernels on the given weight maps (as the reference skips its rasterizer).
     """
+    import torch
+
+    from .regularize import regularize_device
     config = config or Config()
     t0 = time.perf_counter()
     rows = gaussians_array(frame1)
@@ -133,50 +157,51 @@ def compensate_frame(frame1, cameras, tracks, config: Config = None, weightmaps=
         eng.bin(rows, cams, config)
         target, valid = _tracks_arrays(tracks, nv)
         out = eng.compensate(target, valid)
-        import torch
-        torch.cuda.synchronize()
-        status = out.status.cpu().numpy()
-        updates = MotionUpdateList(out.delta_mean.cpu().numpy(), out.rotation.cpu().numpy(),
-                                   out.scale.cpu().numpy(), status)
-        ms = out.motion_status.cpu().numpy().reshape(nv, n)
-        ma = out.motion_a.cpu().numpy().reshape(nv, n, 2, 2)
-        mb = out.motion_b.cpu().numpy().reshape(nv, n, 2)
-        mw = out.weight_sum.cpu().numpy().reshape(nv, n)
-        mc = out.pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
-        msc = out.static_pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
-        msw = out.static_weight_sum.cpu().numpy().reshape(nv, n)
-        motions = [ViewMotionList(v, ms[v], ma[v], mb[v], mw[v], mc[v]) for v in range(nv)]
-        accs = [ViewAccumulators(v, None, None, mw[v], mc[v], msc[v], msw[v]) for v in range(nv)]
+        g_dev = eng._gauss
+        k4 = (out.delta_mean, out.rotation, out.scale, out.status)
+        pc_dev, sc_dev = out.pixel_count, out.static_pixel_count
+        accs = None
+        if callable(regularize):
+            torch.cuda.synchronize()
+            mc = out.pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
+            msc = out.static_pixel_count.cpu().numpy().reshape(nv, n).astype(np.int64)
+            msw = out.static_weight_sum.cpu().numpy().reshape(nv, n)
+            mw = out.weight_sum.cpu().numpy().reshape(nv, n)
+            accs = [ViewAccumulators(v, None, None, mw[v], mc[v], msc[v], msw[v])
+                    for v in range(nv)]
     else:
+        from .engine import as_device
         from .motion2d import accumulate_view, solve_view
         from .multiview import update_all
         accs = [accumulate_view(wm, tf, n, config.static_threshold_px)
                 for wm, tf in zip(weightmaps, tracks)]
         motions = [solve_view(a, config.det_floor, config.min_pixels, config.min_weight)
                    for a in accs]
-        updates = update_all(rows, motions, cams, config.min_views, config.min_total_weight,
-                             config.min_total_pixels, config.eig_floor)
-    if regularize is not None:
+        upd = update_all(rows, motions, cams, config.min_views, config.min_total_weight,
+                         config.min_total_pixels, config.eig_floor)
+        g_dev = as_device(rows, torch.float64)
+        k4 = (as_device(upd.delta_mean, torch.float64), as_device(upd.rotation, torch.float64),
+              as_device(upd.scale, torch.float64), as_device(upd.status, torch.int8))
+        pc_dev = as_device(np.stack([a.pixel_count for a in accs]).astype(np.int32), torch.int32)
+        sc_dev = as_device(np.stack([a.static_pixel_count for a in accs]).astype(np.int32),
+                           torch.int32)
+    if callable(regularize):
+        updates = MotionUpdateList(*(t.cpu().numpy() for t in k4))
         updates = regularize(frame1, updates, accs, config, knn)
-    if isinstance(updates, MotionUpdateList):
-        new_rows = apply_update_rows(rows, updates.delta_mean, updates.rotation, updates.scale,
-                                     updates.status)
-        st = updates.status
-        tallies = {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
-                   "unsolvable": int((st == 0).sum())}
+        k4 = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(g_dev.device)
+                   for a in (updates.delta_mean, updates.rotation, updates.scale,
+                             np.asarray(updates.status, np.int8)))
+        regularize = False
+    if regularize:
+        adj = _knn_adjacency(knn, g_dev, config)
+        *_, status, _flags, new_rows = regularize_device(g_dev, *k4, pc_dev, sc_dev, nv, adj,
+                                                         config)
     else:
-        delta = np.array([u.delta_mean for u in updates]).reshape(n, 3)
-        rot = np.array([u.new_rotation for u in updates]).reshape(n, 4)
-        sc = np.array([u.new_scale for u in updates]).reshape(n, 3)
-        st = np.array([{Status.UNSOLVABLE: 0, Status.SOLVED: 1, Status.STATIC: 2}[u.status]
-                       for u in updates], np.int8)
-        new_rows = apply_update_rows(rows, delta, rot, sc, st)
-        tallies = {"solved": int((st == 1).sum()), "static": int((st == 2).sum()),
-                   "unsolvable": int((st == 0).sum())}
-    dt = time.perf_counter() - t0
-    return FrameResult(frame_index, GaussianList(new_rows), tallies,
-                       {"tracking": 0.0, "compensation": dt, "refinement": 0.0},
-                       compensated_from=first_frame_index)
+        from .regularize import apply_rows_device
+        status = k4[3]
+        new_rows = apply_rows_device(g_dev, *k4)
+    return _result(frame_index, first_frame_index, new_rows.cpu().numpy(), status.cpu().numpy(),
+                   t0)
 
 
 def gausstrack_regularizer():

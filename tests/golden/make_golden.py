@@ -32,6 +32,9 @@ from gausstrack.multiview import (decompose_covariance, solve_covariance3d,  # n
 from gausstrack.errors import GaussTrackError  # noqa: E402
 from gausstrack.scene import generate_scene, oracle_track  # noqa: E402
 from gausstrack.splat import WeightMap, rasterize_weights  # noqa: E402
+from gausstrack import regularize as greg  # noqa: E402
+from gausstrack.core import quat_multiply, quat_normalize  # noqa: E402
+from gausstrack.multiview import MotionUpdate  # noqa: E402
 
 
 def gauss_array(gs):
@@ -311,7 +314,104 @@ def scene_generator_fixture():
     print("scenes", len(d))
 
 
+def _updates_arrays(ups):
+    st = {Status.UNSOLVABLE: 0, Status.SOLVED: 1, Status.STATIC: 2}
+    return (np.array([u.delta_mean for u in ups]), np.array([u.new_rotation for u in ups]),
+            np.array([u.new_scale for u in ups]), np.array([st[u.status] for u in ups], np.int8))
+
+
+def regularize_kats():
+    """build_knn / detect_static_all / median_filter / propagate / apply_updates
+    (regularize.py:37-188) on synthetic update sets, incl. kNN distance ties."""
+    d = {}
+    rng = np.random.default_rng(2604)
+    cases = {}
+    # random cloud with clustered motion; statuses mixed
+    n = 400
+    means = rng.normal(size=(n, 3)) * 2.0
+    cases["cloud"] = means
+    # integer lattice + exact duplicates: many equal distances, ties broken by id
+    g = np.stack(np.meshgrid(np.arange(5), np.arange(5), np.arange(4), indexing="ij"), -1)
+    lat = g.reshape(-1, 3).astype(np.float64) * 0.5
+    lat = np.concatenate([lat, lat[:7]])
+    cases["lattice"] = lat
+    for name, pos in cases.items():
+        n = len(pos)
+        frame1 = [Gaussian3D(pos[i], quat_normalize(rng.normal(size=4)),
+                             rng.uniform(0.05, 0.5, size=3), rng.uniform(0.2, 1.0))
+                  for i in range(n)]
+        ups = []
+        for i, gs in enumerate(frame1):
+            u = rng.random()
+            if u < 0.6:
+                ang = rng.normal(0, 0.05, size=3)
+                half = np.linalg.norm(ang) / 2
+                axis = ang / (np.linalg.norm(ang) + 1e-300)
+                spin = np.concatenate([[np.cos(half)], np.sin(half) * axis])
+                delta = np.array([0.1, -0.05, 0.02]) * (1 + (gs.mean[0] > 0)) + \
+                    rng.normal(0, 0.01, size=3)
+                if rng.random() < 0.05:
+                    delta = rng.normal(0, 2.0, size=3)  # outlier
+                ups.append(MotionUpdate(i, delta, quat_multiply(spin, gs.rotation),
+                                        gs.scale * rng.uniform(0.9, 1.1, size=3), Status.SOLVED))
+            else:
+                ups.append(MotionUpdate(i, np.zeros(3), gs.rotation.copy(), gs.scale.copy(),
+                                        Status.UNSOLVABLE))
+        nv = 4
+        pc = rng.integers(0, 40, size=(n, nv))
+        sc = np.where(rng.random((n, nv)) < 0.3, pc, (pc * rng.random((n, nv))).astype(np.int64))
+        for k in (8, 3):
+            idx = greg.build_knn([gs.mean for gs in frame1], k)
+            d[f"{name}_k{k}_adj"] = idx.adjacency
+        idx = greg.build_knn([gs.mean for gs in frame1], 8)
+        flags = greg.detect_static_all(pc, sc)
+        med = greg.median_filter(ups, idx, frame1)
+        pm = greg.propagate(med, idx, flags, frame1, "mean")
+        pmed = greg.propagate(med, idx, flags, frame1, "median")
+        out = greg.apply_updates(frame1, pm)
+        d[f"{name}_rows"] = gauss_array(frame1)
+        for tag, arr in zip(("delta", "rot", "scale", "status"), _updates_arrays(ups)):
+            d[f"{name}_in_{tag}"] = arr
+        d[f"{name}_pc"], d[f"{name}_sc"], d[f"{name}_flags"] = pc, sc, flags
+        for pre, res in (("med", med), ("pmean", pm), ("pmedian", pmed)):
+            for tag, arr in zip(("delta", "rot", "scale", "status"), _updates_arrays(res)):
+                d[f"{name}_{pre}_{tag}"] = arr
+        d[f"{name}_applied"] = gauss_array(out)
+    np.savez_compressed(os.path.join(OUT, "regularize_kats.npz"), **d)
+    print("regularize_kats", sorted(cases))
+
+
+def compensate_kats():
+    """Full compensate_frame (pipeline.py:110-129: hot path + regularisation tail :88-98) on the
+    scene21 / scene7 fixtures (same scenes and tracks as scene_pipeline)."""
+    from gausstrack.config import Config
+    from gausstrack.pipeline import compensate_frame
+    d = {}
+    for name, scene, noise in [
+            ("scene21", generate_scene(21, 120, 4, 2, mover_fraction=0.25, translate_mag=0.02), 0.0),
+            ("scene7", generate_scene(7, 2000, 8, 2, mover_fraction=0.3, translate_mag=0.02,
+                                      rotate_deg=2.0), 0.5)]:
+        frame1 = scene.frames[0]
+        wms = [rasterize_weights(cam, frame1, view_id=v) for v, cam in enumerate(scene.cameras)]
+        tracks = [trkf_roundtrip(oracle_track(scene, v, 1, noise, seed=0, weightmap=wms[v]))
+                  for v in range(len(scene.cameras))]
+        for avg in ("mean", "median"):
+            res = compensate_frame(frame1, scene.cameras, tracks,
+                                   Config(propagation_average=avg), weightmaps=wms,
+                                   frame_index=1)
+            d[f"{name}_{avg}_rows"] = gauss_array(res.gaussians)
+            d[f"{name}_{avg}_tallies"] = np.array([res.tallies[k] for k in
+                                                   ("solved", "static", "unsolvable")])
+        d[f"{name}_knn"] = greg.build_knn([g.mean for g in frame1], 8).adjacency
+    np.savez_compressed(os.path.join(OUT, "compensate_kats.npz"), **d)
+    print("compensate_kats", {k: v.shape for k, v in d.items()})
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     raster_kats()
     accumulate_kats()
     fuse_kats()

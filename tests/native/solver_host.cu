@@ -2,6 +2,7 @@
 // The product runs the same TS_HD code inside K4 on the GPU; this library lets the CPU suite
 // check the QR / Jacobi / decomposition math against the reference fixtures without a GPU.
 #include "../../paper_2604_02586_b200/csrc/smallsolve.cuh"
+#include "../../paper_2604_02586_b200/csrc/rotation.cuh"
 
 using namespace ts;
 
@@ -59,4 +60,16 @@ extern "C" void host_update_all(const double *G, int64_t n, const ts_camera *cam
   for (int64_t g = 0; g < n; g++)
     st[g] = (int8_t)fuse_gaussian(G + 11 * g, g, n, cams, V, m, *cfg, delta + 3 * g, q + 4 * g,
                                   s + 3 * g);
+}
+
+// rotation.cuh (regularisation helpers), host build
+extern "C" void host_nearest_rotation(const double *m, double *r) { ts::nearest_rotation(m, r); }
+extern "C" void host_sp_from_matrix(const double *m, double *q) { ts::sp_from_matrix(m, q); }
+extern "C" void host_sp_as_euler_xyz(const double *q, double *a) { ts::sp_as_euler_XYZ(q, a); }
+extern "C" void host_sp_euler_xyz_to_matrix(const double *a, double *m) {
+  ts::sp_euler_XYZ_to_matrix(a, m);
+}
+extern "C" void host_matmul3(const double *a, const double *b, double *c) { ts::matmul3(a, b, c); }
+extern "C" void host_matmul3_bt(const double *a, const double *b, double *c) {
+  ts::matmul3_bt(a, b, c);
 }
