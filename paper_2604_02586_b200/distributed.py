@@ -7,7 +7,8 @@ the clip's first-frame Gaussians and its own tracks (pipeline.py:64-65, :177-222
   * target frame f of a clip goes to rank (f - first - 1) mod world (round robin);
   * the frame-1 Gaussians are broadcast from rank 0 once per clip (NCCL broadcast);
   * every rank bins the first frame itself (cheaper than shipping sorted lists, and it mirrors the
-    weight-map reuse of pipeline.py:191-196) and runs K2-K4 for its frames;
+    weight-map reuse of pipeline.py:191-196), builds the clip's kNN, and runs K2-K4 plus the
+    regularisation kernels for its frames;
   * updated Gaussian rows are gathered to rank 0 (NCCL gather).
 
 There is no other data-path collective.  The per-frame arithmetic does not depend on the world
@@ -92,13 +93,19 @@ def compensate_clip_sharded(first_rows, cameras, tracks_by_frame, target_frames,
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     rows = broadcast_rows(first_rows, group)
     if compute is None:
+        from .config import Config
         from .engine import FrameEngine
+        from .regularize import knn_device, regularize_device
+        cfg = config or Config()
         eng = engine or FrameEngine()
-        eng.bin(rows, cameras, config)
+        eng.bin(rows, cameras, cfg)
+        adj = knn_device(eng._gauss, cfg.knn_k)  # once per clip (pipeline.py:197)
 
         def compute(r, cams, target, valid):
             out = eng.compensate(target, valid)
-            return apply_rows(r, out.delta_mean, out.rotation, out.scale, out.status)
+            return regularize_device(eng._gauss, out.delta_mean, out.rotation, out.scale,
+                                     out.status, out.pixel_count, out.static_pixel_count,
+                                     eng.n_views, adj, cfg)[5]
     local = {}
     for f in frames_for_rank(target_frames, rank, world):
         target, valid = tracks_by_frame[f]

@@ -10,8 +10,10 @@
 (pipeline.py:24-29, scene.py:20), so the names are rebound where they are *used*, not only in the
 defining modules.  The shims return the reference's own types (`gausstrack.splat.WeightMap`,
 `gausstrack.motion2d.ViewAccumulators` / `ViewMotion` / `Status`, `gausstrack.core.AffineMotion`,
-`gausstrack.multiview.MotionUpdate`), so the rest of the reference (regularisation, run_pipeline,
-evaluate) keeps working unchanged on top of the GPU results.
+`gausstrack.multiview.MotionUpdate`, `gausstrack.regularize.NeighborIndex`), so the rest of the
+reference (run_pipeline, evaluate, apply_updates) keeps working unchanged on top of the GPU
+results.  The regularisation stages (build_knn, detect_static_all, median_filter, propagate) are
+rebound too, which removes the reference's O(N^2) kNN from compensate_frame.
 """
 
 from __future__ import annotations
@@ -22,7 +24,8 @@ from . import motion2d as _m
 from . import multiview as _mv
 from . import splat as _s
 
-_STAGES = ("rasterize_weights", "accumulate_view", "solve_view", "update_all")
+_STAGES = ("rasterize_weights", "accumulate_view", "solve_view", "update_all", "build_knn",
+           "detect_static_all", "median_filter", "propagate")
 
 
 def _ref_modules():
@@ -33,6 +36,41 @@ def _ref_modules():
     import gausstrack.scene as gs
     import gausstrack.splat as gsp
     return gcore, gm, gmv, gp, gs, gsp
+
+
+def _regularize_shims(gm, gmv):
+    """GPU regularisation stages returning the reference's NeighborIndex / MotionUpdate."""
+    import gausstrack.regularize as greg
+
+    from . import regularize as _r
+    status_of = {0: gm.Status.UNSOLVABLE, 1: gm.Status.SOLVED, 2: gm.Status.STATIC}
+
+    code = {_r.Status.UNSOLVABLE: 0, _r.Status.SOLVED: 1, _r.Status.STATIC: 2}
+
+    def as_ref(updates, new):
+        # entries a stage passed through are the caller's own objects; new ones are converted
+        return [n if n is u else gmv.MotionUpdate(n.gaussian_id, n.delta_mean, n.new_rotation,
+                                                  n.new_scale, status_of[code[n.status]])
+                for u, n in zip(updates, new)]
+
+    def build_knn(positions, k=_r.KNN_K_DEFAULT):
+        idx = _r.build_knn(positions, k)
+        return greg.NeighborIndex(idx.positions, idx.k, idx.adjacency)
+
+    def detect_static_all(pixel_counts, static_counts, min_hit_pixels=_r.MIN_HIT_PIXELS_DEFAULT,
+                          static_fraction=_r.STATIC_FRACTION_DEFAULT,
+                          min_views=_r.STATIC_MIN_VIEWS_DEFAULT):
+        return _r.detect_static_all(pixel_counts, static_counts, min_hit_pixels, static_fraction,
+                                    min_views)
+
+    def median_filter(updates, index, frame1):
+        return as_ref(updates, _r.median_filter(updates, index, frame1))
+
+    def propagate(updates, index, static_flags, frame1, average="mean"):
+        return as_ref(updates, _r.propagate(updates, index, static_flags, frame1, average))
+
+    return dict(build_knn=build_knn, detect_static_all=detect_static_all,
+                median_filter=median_filter, propagate=propagate)
 
 
 def make_shims():
@@ -69,7 +107,7 @@ def make_shims():
                 for i in range(len(ul))]
 
     return dict(rasterize_weights=rasterize_weights, accumulate_view=accumulate_view,
-                solve_view=solve_view, update_all=update_all)
+                solve_view=solve_view, update_all=update_all, **_regularize_shims(gm, gmv))
 
 
 def to_reference_motions(vml, gm, gcore):
@@ -88,11 +126,14 @@ def to_reference_motions(vml, gm, gcore):
 def install():
     """Rebind the four stage names in gausstrack.pipeline / gausstrack.scene (and the defining
     modules).  Returns a handle for `uninstall`."""
+    import gausstrack.regularize as greg
     _, gm, gmv, gp, gs, gsp = _ref_modules()
     shims = make_shims()
     saved = []
     targets = {"rasterize_weights": (gp, gs, gsp), "accumulate_view": (gp, gm),
-               "solve_view": (gp, gm), "update_all": (gp, gmv)}
+               "solve_view": (gp, gm), "update_all": (gp, gmv), "build_knn": (gp, greg),
+               "detect_static_all": (gp, greg), "median_filter": (gp, greg),
+               "propagate": (gp, greg)}
     for name, mods in targets.items():
         for mod in mods:
             if hasattr(mod, name):

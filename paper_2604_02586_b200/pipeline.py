@@ -13,8 +13,10 @@ pipeline.py:88-98, regularize.py:37-188) runs as two more kernels on the K4 outp
 
 from __future__ import annotations
 
+import csv
+import io
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -234,3 +236,195 @@ def gausstrack_regularizer():
                                 np.array([code[u.status] for u in ups], np.int8))
 
     return run
+
+
+# -- clip driver (pipeline.py:132-237) -----------------------------------------------------------
+
+def _scene_arrays(scene):
+    """SceneArrays view of our SceneArrays or the reference's SceneSequence (object frames)."""
+    from .scene import SceneArrays
+    if isinstance(scene, SceneArrays):
+        return scene
+    frames = [gaussians_array(f) for f in scene.frames]
+    return SceneArrays(list(scene.cameras), frames, None, None)
+
+
+def _zero_result(frame, rows):
+    return FrameResult(frame, GaussianList(rows), {"solved": 0, "static": 0, "unsolvable": 0},
+                       {"tracking": 0.0, "compensation": 0.0, "refinement": 0.0})
+
+
+def _share_clip_results(results, clip, n, group):
+    """All-gather the FrameResults of a clip's target frames (rows over NCCL, metadata as
+    objects); each frame is owned by one rank (distributed.frames_for_rank)."""
+    import torch
+    import torch.distributed as dist
+
+    from .distributed import frames_for_rank
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per_rank = [frames_for_rank(clip.target_frames, r, world) for r in range(world)]
+    slots = max(len(p) for p in per_rank)
+    if slots == 0:
+        return
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.zeros((slots, n, 11), dtype=torch.float64, device=dev)
+    meta = []
+    for i, f in enumerate(per_rank[rank]):
+        r = results[f]
+        buf[i] = torch.from_numpy(np.ascontiguousarray(r.gaussians.rows)).to(dev)
+        meta.append((f, r.tallies, r.wall_time, r.compensated_from))
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    metas = [None] * world
+    dist.all_gather_object(metas, meta, group=group)
+    for r in range(world):
+        for i, (f, tallies, wall, src) in enumerate(metas[r]):
+            results[f] = FrameResult(f, GaussianList(bufs[r][i].cpu().numpy()), tallies, wall,
+                                     compensated_from=src)
+
+
+def run_pipeline(scene, clip_len, workers=1, config: Config = None, mode="short",
+                 noise_sigma_px=0.0, seed=0, refine_hook=None, stage_totals=None, group=None):
+    """Tracking + compensation over every clip of a scene (pipeline.py:132-237) on the GPU.
+
+    Per clip: the tracker's binning of the ground-truth first frame (K1) is reused for the
+    compensation when the clip starts from ground truth (short mode, or the first clip of a
+    chain) -- the reference's weight-map reuse (:191-196); the exact kNN is built once per clip on
+    the device; every target frame then runs the GPU oracle tracker, K2-K4 and the regularisation
+    kernels.  Long mode chains clips through the previous clip's estimate of its last frame.
+
+    `workers` is accepted for signature parity (>= 1); parallelism comes from the GPU and, when
+    torch.distributed is initialised with more than one rank (`group`), from frame sharding:
+    target frames are dealt round robin to ranks and every rank ends with the full result list
+    (all-gather per clip, so long-mode chains see the previous clip's last frame).  Results do
+    not depend on the world size.  stage_totals accumulates setup / tracking / fuse seconds.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .distributed import frames_for_rank
+    from .engine import FrameEngine
+    from .regularize import knn_device, regularize_device
+    from .scene import oracle_tracks
+    if workers < 1:
+        raise InvalidConfig(f"workers must be >= 1, got {workers}")
+    config = config or Config()
+    if stage_totals is None:
+        stage_totals = {}
+    stage_totals.update({"setup": 0.0, "tracking": 0.0, "fuse": 0.0})
+    scene = _scene_arrays(scene)
+    cams = cameras_array(scene.cameras)
+    nv = len(cams)
+    clips = segment_clips(scene.n_frames, clip_len, nv, mode)
+    sharded = dist.is_initialized() and dist.get_world_size(group) > 1
+    world = dist.get_world_size(group) if sharded else 1
+    rank = dist.get_rank(group) if sharded else 0
+
+    results = {0: _zero_result(0, scene.frames[0])}
+    eng_track, eng_comp = FrameEngine(), None
+    for clip in clips:
+        gt_first = scene.frames[clip.first_frame]
+        if mode == "short":
+            first_rows = gt_first
+            results.setdefault(clip.first_frame, _zero_result(clip.first_frame, gt_first))
+        else:
+            first_rows = results[clip.first_frame].gaussians.rows
+        if not clip.target_frames:
+            continue
+        t0 = time.perf_counter()
+        eng_track.bin(gt_first, cams, config)
+        if first_rows is gt_first or np.array_equal(first_rows, gt_first):
+            eng = eng_track
+        else:
+            eng_comp = eng_comp or FrameEngine()
+            eng = eng_comp.bin(first_rows, cams, config)
+        g_dev = eng._gauss
+        adj = knn_device(g_dev, config.knn_k)
+        torch.cuda.synchronize()
+        stage_totals["setup"] += time.perf_counter() - t0
+        for f in frames_for_rank(clip.target_frames, rank, world):
+            t0 = time.perf_counter()
+            tgt, val = oracle_tracks(scene, f, noise_sigma_px, seed, first_frame=clip.first_frame,
+                                     engine=eng_track)
+            torch.cuda.synchronize()
+            t_track = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            out = eng.compensate(tgt, val)
+            *_, status, _flags, rows = regularize_device(
+                g_dev, out.delta_mean, out.rotation, out.scale, out.status, out.pixel_count,
+                out.static_pixel_count, nv, adj, config)
+            rows_h, st = rows.cpu().numpy(), status.cpu().numpy()
+            t_comp = time.perf_counter() - t0
+            res = _result(f, clip.first_frame, rows_h, st, t0)
+            res.wall_time.update(tracking=t_track, compensation=t_comp)
+            if refine_hook is not None:
+                t0 = time.perf_counter()
+                res.gaussians = refine_hook(res.frame, res.gaussians)
+                res.wall_time["refinement"] = time.perf_counter() - t0
+            stage_totals["tracking"] += t_track
+            stage_totals["fuse"] += t_comp
+            results[f] = res
+        if sharded:
+            _share_clip_results(results, clip, len(first_rows), group)
+    return [results[f] for f in sorted(results)]
+
+
+# -- evaluation (pipeline.py:243-298) ------------------------------------------------------------
+
+CSV_COLUMNS = ["frame", "mean_pos_err", "p95_pos_err", "mean_rot_err_deg", "mean_rel_scale_err",
+               "n_solved", "n_static", "n_unsolvable", "t_track", "t_comp", "t_refine"]
+
+
+@dataclass
+class EvaluationReport:
+    rows: list = field(default_factory=list)
+
+    def write_csv(self, path):
+        with open(path, "w", newline="") as fh:
+            w = csv.DictWriter(fh, fieldnames=CSV_COLUMNS)
+            w.writeheader()
+            w.writerows(self.rows)
+
+    def summary(self):
+        out = io.StringIO()
+        out.write(f"{'frame':>6} {'pos_err':>12} {'p95_pos':>12} {'rot_deg':>10} "
+                  f"{'scale_rel':>10} {'solved':>7} {'static':>7} {'unsolv':>7}\n")
+        for r in self.rows:
+            out.write(f"{r['frame']:>6} {r['mean_pos_err']:>12.6g} {r['p95_pos_err']:>12.6g} "
+                      f"{r['mean_rot_err_deg']:>10.4g} {r['mean_rel_scale_err']:>10.4g} "
+                      f"{r['n_solved']:>7} {r['n_static']:>7} {r['n_unsolvable']:>7}\n")
+        return out.getvalue()
+
+
+def _unit_rows(q):
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+def evaluate(results, scene) -> EvaluationReport:
+    """Ground-truth error per frame: position, rotation (geodesic, degrees), relative scale
+    (pipeline.py:273-298), vectorised over the Gaussians."""
+    scene = _scene_arrays(scene)
+    report = EvaluationReport()
+    for res in results:
+        est = gaussians_array(res.gaussians)
+        truth = scene.frames[res.frame]
+        pos_err = np.linalg.norm(est[:, 0:3] - truth[:, 0:3], axis=1)
+        d = np.abs(np.sum(_unit_rows(est[:, 3:7]) * _unit_rows(truth[:, 3:7]), axis=1))
+        rot_err = 2.0 * np.arccos(np.minimum(d, 1.0))
+        scale_err = np.mean(np.abs(est[:, 7:10] - truth[:, 7:10]) / truth[:, 7:10], axis=1)
+        report.rows.append({
+            "frame": res.frame,
+            "mean_pos_err": float(np.mean(pos_err)),
+            "p95_pos_err": float(np.percentile(pos_err, 95)),
+            "mean_rot_err_deg": float(np.degrees(np.mean(rot_err))),
+            "mean_rel_scale_err": float(np.mean(scale_err)),
+            "n_solved": res.tallies["solved"],
+            "n_static": res.tallies["static"],
+            "n_unsolvable": res.tallies["unsolvable"],
+            "t_track": res.wall_time["tracking"],
+            "t_comp": res.wall_time["compensation"],
+            "t_refine": res.wall_time["refinement"],
+        })
+    return report

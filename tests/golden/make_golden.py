@@ -407,6 +407,27 @@ def compensate_kats():
     print("compensate_kats", {k: v.shape for k, v in d.items()})
 
 
+def pipeline_kats():
+    """run_pipeline (pipeline.py:132-237) on the reference's test scene (tests/test_pipeline.py:
+    50-52): short / long clips, clean and noisy tracks."""
+    from gausstrack.pipeline import run_pipeline
+    d = {}
+    scene = generate_scene(13, 80, 4, 4, mover_fraction=0.25, translate_mag=0.02)
+    d["frames"] = np.stack([gauss_array(f) for f in scene.frames])
+    d["cameras"] = cam_array(scene.cameras)
+    for tag, kw in [("short3", dict(clip_len=3, mode="short")),
+                    ("long2", dict(clip_len=2, mode="long")),
+                    ("short9_noisy", dict(clip_len=9, mode="short", noise_sigma_px=0.5))]:
+        res = run_pipeline(scene, workers=1, **kw)
+        d[f"{tag}_rows"] = np.stack([gauss_array(r.gaussians) for r in res])
+        d[f"{tag}_tallies"] = np.array([[r.tallies[k] for k in ("solved", "static", "unsolvable")]
+                                        for r in res])
+        d[f"{tag}_from"] = np.array([-1 if r.compensated_from is None else r.compensated_from
+                                     for r in res])
+    np.savez_compressed(os.path.join(OUT, "pipeline_kats.npz"), **d)
+    print("pipeline_kats", {k: v.shape for k, v in d.items()})
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:

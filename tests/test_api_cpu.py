@@ -159,3 +159,21 @@ def test_scene_generator_rejects_bad_configs():
         generate_scene(0, 100, 2, 2)
     with pytest.raises(errors.InvalidConfig):
         generate_scene(0, 100, 4, 2, focal=5000)
+
+
+def test_evaluate_perfect_results_zero_error():
+    """evaluate (pipeline.py:273-298) is host-side reporting: exact results have zero error
+    (reference tests/test_pipeline.py:142-154)."""
+    from paper_2604_02586_b200.pipeline import FrameResult, GaussianList, evaluate
+    from paper_2604_02586_b200.scene import generate_scene
+    s = generate_scene(13, 80, 4, 4, mover_fraction=0.25, translate_mag=0.02)
+    results = [FrameResult(t, GaussianList(s.frames[t]), {"solved": 0, "static": 0,
+                                                          "unsolvable": 0},
+                           {"tracking": 0, "compensation": 0, "refinement": 0})
+               for t in range(s.n_frames)]
+    report = evaluate(results, s)
+    assert len(report.rows) == s.n_frames
+    for row in report.rows:
+        assert row["mean_pos_err"] == pytest.approx(0.0, abs=1e-12)
+        assert row["mean_rot_err_deg"] == pytest.approx(0.0, abs=1e-5)
+        assert row["mean_rel_scale_err"] == pytest.approx(0.0, abs=1e-12)

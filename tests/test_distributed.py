@@ -79,3 +79,39 @@ def test_sharded_equals_serial(tmp_path):
         np.testing.assert_array_equal(got[str(f)], serial[f])
     # the motion actually moved something
     assert np.abs(serial[1][:, 0:3] - rows[:, 0:3]).max() > 0
+
+
+def _share_worker(rank, world, port, out_path):
+    from paper_2604_02586_b200.pipeline import Clip, FrameResult, GaussianList, _share_clip_results
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    clip = Clip(0, (1, 2, 3, 4, 5), (0, 1))
+    results = {}
+    for f in frames_for_rank(clip.target_frames, rank, world):
+        rows = np.full((6, 11), float(f)) + np.arange(11)
+        results[f] = FrameResult(f, GaussianList(rows), {"solved": f, "static": 0,
+                                                         "unsolvable": 6 - f},
+                                 {"tracking": 0.1 * f, "compensation": 0.0, "refinement": 0.0},
+                                 compensated_from=0)
+    _share_clip_results(results, clip, 6, None)
+    np.savez(f"{out_path}.{rank}.npz",
+             **{str(f): results[f].gaussians.rows for f in results},
+             tallies=np.array([results[f].tallies["solved"] for f in sorted(results)]),
+             src=np.array([results[f].compensated_from for f in sorted(results)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_run_pipeline_result_sharing(tmp_path):
+    """run_pipeline's per-clip all-gather: every rank ends with every frame (long-mode chains
+    need the previous clip's last frame everywhere)."""
+    out = str(tmp_path / "share")
+    mp.spawn(_share_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for rank in range(2):
+        got = np.load(f"{out}.{rank}.npz")
+        assert sorted(int(k) for k in got.files if k.isdigit()) == [1, 2, 3, 4, 5]
+        for f in range(1, 6):
+            np.testing.assert_array_equal(got[str(f)], np.full((6, 11), float(f)) + np.arange(11))
+        np.testing.assert_array_equal(got["tallies"], [1, 2, 3, 4, 5])
+        np.testing.assert_array_equal(got["src"], [0] * 5)

@@ -285,7 +285,7 @@ def test_compensate_frame_api():
     cams = [camera_from_row(r) for r in d["cameras"]]
     h, w = valid.shape[1:]
     tracks = [TrackField(v, w, h, target[v], valid[v]) for v in range(len(cams))]
-    res = compensate_frame(frame1, cams, tracks, Config(), frame_index=1)
+    res = compensate_frame(frame1, cams, tracks, Config(), frame_index=1, regularize=False)
     assert res.frame == 1 and len(res.gaussians) == len(frame1)
     assert sum(res.tallies.values()) == len(frame1)
     assert res.tallies["solved"] == int(d["u_status"].sum())

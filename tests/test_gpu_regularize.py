@@ -167,3 +167,4 @@ def test_compensate_frame_vs_reference(kats, scene, avg):
     rows = res.gaussians.rows
     # SURVEY §8(c) contract: means rel 1e-4, rotations 1e-3 rad; observed ~1e-9 (hot-path ulps)
     np.testing.assert_allclose(rows, ref[f"{scene}_{avg}_rows"], rtol=1e-7, atol=5e-9)
+
