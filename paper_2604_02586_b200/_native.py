@@ -16,7 +16,8 @@ import numpy as np
 from .errors import DimensionMismatch, GaussTrackError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtrackersplat_b200.so")
+# TS_LIB_PATH selects an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(_HERE, "_lib", "libtrackersplat_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 TS_OK = 0

@@ -66,7 +66,7 @@ struct ts_plan {
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
   // regularisation buffers
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
-      reg_static, reg_source, reg_euler;
+      reg_static, reg_source, reg_euler, k4_ws;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
   int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
@@ -120,7 +120,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end,
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
-                          &p->reg_source, &p->reg_euler};
+                          &p->reg_source, &p->reg_euler, &p->k4_ws};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -137,7 +137,7 @@ void release_all(ts_plan *p) {
                     &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
-                    &p->reg_static, &p->reg_source, &p->reg_euler};
+                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -464,8 +464,10 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 
+  ENSURE(p->k4_ws, k4_workspace_bytes(n));
   cudaEvent_t e5 = p->mark_begin(s);
-  launch_k4_fuse(p->gaussians, n, ptr<ts_camera>(p->cams), p->V, m, p->cfg, *updates, s);
+  launch_k4_fuse(p->gaussians, n, ptr<ts_camera>(p->cams), p->V, m, p->cfg, *updates,
+                 p->k4_ws.p, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_FUSE, e5, s);
   return TS_OK;
@@ -633,13 +635,15 @@ int ts_update_all(const double *gaussians, int64_t n, const ts_camera *cameras, 
   cudaStream_t s = (cudaStream_t)stream;
   if (!cameras || n_views < 1 || !motions || !config || !updates || n < 0)
     return TS_E_INVALID_ARGUMENT;
-  void *dcams = nullptr;
+  void *dcams = nullptr, *ws = nullptr;
   TS_CUDA_TRY(cudaMallocAsync(&dcams, sizeof(ts_camera) * n_views, s));
+  TS_CUDA_TRY(cudaMallocAsync(&ws, k4_workspace_bytes(n), s));
   TS_CUDA_TRY(cudaMemcpyAsync(dcams, cameras, sizeof(ts_camera) * n_views, cudaMemcpyHostToDevice, s));
   launch_k4_fuse(gaussians, n, reinterpret_cast<ts_camera *>(dcams), n_views, *motions, *config,
-                 *updates, s);
+                 *updates, ws, s);
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(dcams, s);
+  cudaFreeAsync(ws, s);
   return e == cudaSuccess ? TS_OK : TS_E_CUDA;
 }
 

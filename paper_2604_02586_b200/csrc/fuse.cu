@@ -9,29 +9,33 @@
 //     rotations, every vech block + rhs (:226-229) into a 6x6 R and Q^T b.  QR keeps the singular
 //     values and right singular vectors of the stacked matrix, so the reference's SVD-based tests
 //     (s[-2]-s[-1] <= 1e-9 s[0]; |x3| <= 1e-9 |x|; s[-1] < 1e-9 s[0]) are taken on R;
-//   * one-sided Jacobi SVD of R (high relative accuracy for the small singular values the
-//     degeneracy tests look at), back substitution for the covariance least squares;
+//   * the degeneracy tests are decided by rigorous certificates on R where possible (inverse
+//     iteration null vector + interlacing bound for the DLT gap; 1/(|R|_F |R^-1|_F) for the rank
+//     test); the Gaussians they cannot decide are queued and finished by k4_finish with a
+//     one-sided Jacobi SVD of R (high relative accuracy for the small singular values), so the
+//     SVD never diverges a warp of k4_fuse; back substitution for the least squares;
 //   * cyclic Jacobi for the 3x3 eigenproblem, then the reference's discrete choices verbatim:
 //     first-maximum permutation in itertools order, sign flips, det repair, matrix_to_quat.
 #include <float.h>
+
+#include <algorithm>
+
 #include "smallsolve.cuh"
 
 namespace ts {
 
 
-__global__ void __launch_bounds__(128, 3) k4_fuse(const double *__restrict__ G, int64_t n,
-                                               const ts_camera *__restrict__ cams, int V,
-                                               ts_motions m, ts_config cfg, ts_updates u) {
-  extern __shared__ ts_camera s_cam4[];
-  for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam4[i] = cams[i];
-  __syncthreads();
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
-  double gs[11];
-#pragma unroll
-  for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
-  double delta[3], q[4], sc[3];
-  const int status = fuse_gaussian(gs, g, n, s_cam4, V, m, cfg, delta, q, sc);
+// Deferred slow-path record: the R factors of a Gaussian whose triangulation-gap or rank decision
+// needs an SVD (a few percent of Gaussians, but enough to put an SVD into almost every warp).
+struct K4Deferred {
+  double r4[10];  // upper triangle of R4, row-major
+  double r6[21];  // upper triangle of R6
+  double c6[6];
+  int64_t g;
+};
+
+__device__ __forceinline__ void store_updates(ts_updates u, int64_t g, const double *delta,
+                                              const double *q, const double *sc, int status) {
 #pragma unroll
   for (int i = 0; i < 3; i++) {
     u.delta_mean[3 * g + i] = delta[i];
@@ -40,6 +44,80 @@ __global__ void __launch_bounds__(128, 3) k4_fuse(const double *__restrict__ G, 
 #pragma unroll
   for (int i = 0; i < 4; i++) u.rotation[4 * g + i] = q[i];
   u.status[g] = (int8_t)status;
+}
+
+#ifndef TS_K4_MIN_BLOCKS
+#define TS_K4_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *__restrict__ G, int64_t n,
+                                               const ts_camera *__restrict__ cams, int V,
+                                               ts_motions m, ts_config cfg, ts_updates u,
+                                               K4Deferred *defer, unsigned *n_defer) {
+  extern __shared__ ts_camera s_cam4[];
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam4[i] = cams[i];
+  __syncthreads();
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  double gs[11];
+#pragma unroll
+  for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
+  double delta[3], q[4], sc[3], R4[4][4], R6[6][6], c6[6];
+  const int status = fuse_gaussian(gs, g, n, s_cam4, V, m, cfg, delta, q, sc, R4, R6, c6, false);
+  if (status == TS_FUSE_DEFER_STATUS) {
+    K4Deferred *d = defer + atomicAdd(n_defer, 1u);
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = i; j < 4; j++) d->r4[k++] = R4[i][j];
+    k = 0;
+#pragma unroll
+    for (int i = 0; i < 6; i++)
+#pragma unroll
+      for (int j = i; j < 6; j++) d->r6[k++] = R6[i][j];
+#pragma unroll
+    for (int i = 0; i < 6; i++) d->c6[i] = c6[i];
+    d->g = g;
+    return;
+  }
+  store_updates(u, g, delta, q, sc, status);
+}
+
+// The deferred Gaussians, with the SVD decisions (same code path as the host build).
+__global__ void __launch_bounds__(128) k4_finish(const double *__restrict__ G, ts_config cfg,
+                                                 ts_updates u, const K4Deferred *defer,
+                                                 const unsigned *n_defer) {
+  const unsigned cnt = *n_defer;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const K4Deferred &d = defer[i];
+    const int64_t g = d.g;
+    double gs[11];
+#pragma unroll
+    for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
+    double R4[4][4], R6[6][6], c6[6];
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) R4[a][b] = b >= a ? d.r4[k++] : 0.0;
+    k = 0;
+#pragma unroll
+    for (int a = 0; a < 6; a++)
+#pragma unroll
+      for (int b = 0; b < 6; b++) R6[a][b] = b >= a ? d.r6[k++] : 0.0;
+#pragma unroll
+    for (int a = 0; a < 6; a++) c6[a] = d.c6[a];
+    double delta[3], q[4], sc[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      delta[a] = 0.0;
+      sc[a] = gs[7 + a];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) q[a] = gs[3 + a];
+    const int status = fuse_finish(gs, R4, R6, c6, cfg, delta, q, sc, true);
+    store_updates(u, g, delta, q, sc, status);
+  }
 }
 
 __global__ void k_triangulate_batch(const double *__restrict__ rows, const int32_t *__restrict__ nr,
@@ -127,9 +205,18 @@ void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, t
                      const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s) {
   k4_debug<<<1, 1, 0, s>>>(G, n, cams, V, m, cfg, g, dbg);
 }
+size_t k4_workspace_bytes(int64_t n) { return 256 + sizeof(K4Deferred) * (size_t)n; }
+
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                    const ts_config &cfg, ts_updates u, cudaStream_t s) {
-  if (n) k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u);
+                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s) {
+  if (!n) return;
+  unsigned *n_defer = reinterpret_cast<unsigned *>(workspace);
+  K4Deferred *defer = reinterpret_cast<K4Deferred *>(reinterpret_cast<char *>(workspace) + 256);
+  cudaMemsetAsync(n_defer, 0, sizeof(unsigned), s);
+  k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u, defer,
+                                                              n_defer);
+  const unsigned fin_blocks = (unsigned)std::min<int64_t>(blocks(n, 128), 148 * 4);
+  k4_finish<<<fin_blocks, 128, 0, s>>>(G, cfg, u, defer, n_defer);
 }
 void launch_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch,
                               int max_rows, double *x, int8_t *status, cudaStream_t s) {

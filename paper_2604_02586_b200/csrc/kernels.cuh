@@ -49,8 +49,9 @@ void launch_accumulate(int64_t n, const uint32_t *seg_start, const uint32_t *seg
                        double *wsum, int64_t *cnt, int64_t *scnt, double *swsum, cudaStream_t s);
 
 // K4: multi-view fuse (update_all)
+size_t k4_workspace_bytes(int64_t n);
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                    const ts_config &cfg, ts_updates u, cudaStream_t s);
+                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s);
 void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
                      const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s);
 void launch_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch,

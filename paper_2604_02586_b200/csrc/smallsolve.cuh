@@ -11,6 +11,12 @@
 
 namespace ts {
 
+// tri-state result of the fuse's solve steps: the slow (SVD) decision can be deferred to a second
+// kernel so that the rare near-degenerate Gaussians do not stall whole warps of K4
+#define TS_FUSE_FAIL 0
+#define TS_FUSE_OK 1
+#define TS_FUSE_DEFER 2
+
 template <int N>
 TS_HD void qr_add_row(double (&R)[N][N], double (&row)[N]) {
 #pragma unroll
@@ -111,8 +117,108 @@ TS_HD void jacobi_svd(double (&B)[N][N], double (&V)[N][N], double (&s)[N]) {
   }
 }
 
-// triangulate_mean from the R factor of the stacked DLT rows (multiview.py:249-257).
-TS_HD bool triangulate_from_r(const double (&R)[4][4], double *mean) {
+// Right singular vector of the smallest singular value of an upper-triangular 4x4 R by inverse
+// iteration on R^T R (two triangular solves per step, error ratio (s3/s2)^2 per step), started from
+// R^-1 e3.  Returns false (caller falls back to the Jacobi SVD) on a zero pivot or if 12 steps do
+// not converge to 4 ulp.
+TS_HD bool null_vector_r4(const double (&R)[4][4], double (&x)[4]) {
+  if (!(R[0][0] != 0.0 && R[1][1] != 0.0 && R[2][2] != 0.0 && R[3][3] != 0.0)) return false;
+  double y[4];
+  y[3] = 1.0 / R[3][3];
+  y[2] = -(R[2][3] * y[3]) / R[2][2];
+  y[1] = -(R[1][2] * y[2] + R[1][3] * y[3]) / R[1][1];
+  y[0] = -(R[0][1] * y[1] + R[0][2] * y[2] + R[0][3] * y[3]) / R[0][0];
+  double inv = rsqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2] + y[3] * y[3]);
+#pragma unroll
+  for (int i = 0; i < 4; i++) x[i] = y[i] * inv;
+  for (int it = 0; it < 12; it++) {
+    double z[4];  // R^T z = x (forward), then R y = z (back)
+    z[0] = x[0] / R[0][0];
+    z[1] = (x[1] - R[0][1] * z[0]) / R[1][1];
+    z[2] = (x[2] - R[0][2] * z[0] - R[1][2] * z[1]) / R[2][2];
+    z[3] = (x[3] - R[0][3] * z[0] - R[1][3] * z[1] - R[2][3] * z[2]) / R[3][3];
+    y[3] = z[3] / R[3][3];
+    y[2] = (z[2] - R[2][3] * y[3]) / R[2][2];
+    y[1] = (z[1] - R[1][2] * y[2] - R[1][3] * y[3]) / R[1][1];
+    y[0] = (z[0] - R[0][1] * y[1] - R[0][2] * y[2] - R[0][3] * y[3]) / R[0][0];
+    const double nn = y[0] * y[0] + y[1] * y[1] + y[2] * y[2] + y[3] * y[3];
+    if (!(nn > 0.0 && nn < 1e300)) return false;
+    inv = rsqrt(nn);
+    if (y[0] * x[0] + y[1] * x[1] + y[2] * x[2] + y[3] * x[3] < 0) inv = -inv;
+    double diff = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const double v = y[i] * inv;
+      diff = fmax(diff, fabs(v - x[i]));
+      x[i] = v;
+    }
+    if (diff <= 4.5e-16) return true;
+  }
+  return false;
+}
+
+// Certificate for the reference's gap test s[-2] - s[-1] > 1e-9 s[0] (multiview.py:251) given an
+// approximate null vector x (unit) of R: s[-1] <= |R x| (+ rounding), s[0] <= |R|_F, and s[-2] >=
+// sigma_min(R restricted to x-perp) >= 1/|R'^-1|_F, R' the 3x3 R factor of R H[:, 0:3] with H
+// the Householder reflector taking x to the last axis (Cauchy interlacing).  true => the test
+// passes for certain; false => undecided (run the SVD).
+TS_HD bool gap_certified(const double (&R)[4][4], const double (&x)[4]) {
+  double nf2 = 0.0, rx2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    double rxi = 0.0;
+#pragma unroll
+    for (int j = i; j < 4; j++) {
+      nf2 = fma(R[i][j], R[i][j], nf2);
+      rxi = fma(R[i][j], x[j], rxi);
+    }
+    rx2 = fma(rxi, rxi, rx2);
+  }
+  const double nf = sqrt(nf2);
+  const double s3u = sqrt(rx2) + 8e-16 * nf;
+  // w = x + sign(x3) e3; H = I - 2 w w^T / (w^T w); columns 0..2 of R H span R (x-perp)
+  const double sg = x[3] < 0 ? -1.0 : 1.0;
+  const double w[4] = {x[0], x[1], x[2], x[3] + sg};
+  const double ww = w[0] * w[0] + w[1] * w[1] + w[2] * w[2] + w[3] * w[3];
+  double Rp[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    double rw = 0.0;
+#pragma unroll
+    for (int j = i; j < 4; j++) rw = fma(R[i][j], w[j], rw);
+    const double f = 2.0 * rw / ww;
+    double row[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) row[j] = ((j >= i) ? R[i][j] : 0.0) - f * w[j];
+    qr_add_row<3>(Rp, row);
+  }
+  if (!(Rp[0][0] != 0.0 && Rp[1][1] != 0.0 && Rp[2][2] != 0.0)) return false;
+  // |R'^-1|_F^2 by back substitution on the three unit vectors
+  const double i00 = 1.0 / Rp[0][0], i11 = 1.0 / Rp[1][1], i22 = 1.0 / Rp[2][2];
+  const double i01 = -Rp[0][1] * i11 * i00;
+  const double i12 = -Rp[1][2] * i22 * i11;
+  const double i02 = -(Rp[0][1] * i12 + Rp[0][2] * i22) * i00;
+  const double inv2 = i00 * i00 + i11 * i11 + i22 * i22 + i01 * i01 + i12 * i12 + i02 * i02;
+  const double lb = rsqrt(inv2) * (1.0 - 1e-12);
+  return lb - s3u > TS_SINGULAR_GAP_REL * nf * (1.0 + 1e-12);
+}
+
+// triangulate_mean from the R factor of the stacked DLT rows (multiview.py:249-257).  Fast path:
+// inverse-iteration null vector + a rigorous certificate for the singular-gap test; the one-sided
+// Jacobi SVD (below) decides only when the certificate cannot (near-degenerate geometry).
+TS_HD int triangulate_from_r(const double (&R)[4][4], double *mean, bool allow_slow = true) {
+  {
+    double x[4];
+    if (null_vector_r4(R, x) && gap_certified(R, x)) {
+      // x is unit: the solution-at-infinity test (:255) is |x3| > 1e-9
+      if (!(fabs(x[3]) > TS_SINGULAR_GAP_REL)) return TS_FUSE_FAIL;
+      mean[0] = x[0] / x[3];
+      mean[1] = x[1] / x[3];
+      mean[2] = x[2] / x[3];
+      return TS_FUSE_OK;
+    }
+  }
+  if (!allow_slow) return TS_FUSE_DEFER;
   double B[4][4], V[4][4], s[4];
 #pragma unroll
   for (int i = 0; i < 4; i++)
@@ -136,7 +242,7 @@ TS_HD bool triangulate_from_r(const double (&R)[4][4], double *mean) {
       }
   const double s0 = v[0], s2 = v[2], s3 = v[3];
   const int imin = id[3];
-  if (!(s2 - s3 > TS_SINGULAR_GAP_REL * s0)) return false;
+  if (!(s2 - s3 > TS_SINGULAR_GAP_REL * s0)) return TS_FUSE_FAIL;
   double x[4];
 #pragma unroll
   for (int i = 0; i < 4; i++) {
@@ -146,16 +252,16 @@ TS_HD bool triangulate_from_r(const double (&R)[4][4], double *mean) {
       if (j == imin) x[i] = V[i][j];
   }
   const double nrm = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3]);
-  if (!(fabs(x[3]) > TS_SINGULAR_GAP_REL * nrm)) return false;
+  if (!(fabs(x[3]) > TS_SINGULAR_GAP_REL * nrm)) return TS_FUSE_FAIL;
   mean[0] = x[0] / x[3];
   mean[1] = x[1] / x[3];
   mean[2] = x[2] / x[3];
-  return true;
+  return TS_FUSE_OK;
 }
 
 // solve_covariance3d from R (6x6) and Q^T b (multiview.py:259-263).
-TS_HD bool cov_from_r(const double (&R)[6][6], const double (&c6)[6],
-                                           double *sol) {
+TS_HD int cov_from_r(const double (&R)[6][6], const double (&c6)[6], double *sol,
+                     bool allow_slow = true) {
   // Rigorous cheap bound first: s_max <= |R|_F and s_min >= 1/|R^-1|_F, so
   // 1/(|R|_F |R^-1|_F) >= 1e-9 proves the reference's rank test passes; only otherwise run the
   // one-sided Jacobi SVD to take the exact decision.
@@ -185,6 +291,7 @@ TS_HD bool cov_from_r(const double (&R)[6][6], const double (&c6)[6],
       need_svd = !(1.0 >= 1.0000001 * TS_SINGULAR_GAP_REL * sqrt(fro * finv));
     }
   }
+  if (need_svd && !allow_slow) return TS_FUSE_DEFER;
   if (need_svd) {
     double B[6][6], s[6];
     double Vd[6][6];
@@ -199,7 +306,7 @@ TS_HD bool cov_from_r(const double (&R)[6][6], const double (&c6)[6],
       smax = fmax(smax, s[j]);
       smin = fmin(smin, s[j]);
     }
-    if (!(smin >= TS_SINGULAR_GAP_REL * smax)) return false;
+    if (!(smin >= TS_SINGULAR_GAP_REL * smax)) return TS_FUSE_FAIL;
   }
 #pragma unroll
   for (int i = 5; i >= 0; i--) {
@@ -208,7 +315,7 @@ TS_HD bool cov_from_r(const double (&R)[6][6], const double (&c6)[6],
     for (int k = i + 1; k < 6; k++) acc -= R[i][k] * sol[k];
     sol[i] = acc / R[i][i];
   }
-  return true;
+  return TS_FUSE_OK;
 }
 
 // Cyclic Jacobi eigen-decomposition of a symmetric 3x3; eigenvalues ascending (as eigh).
@@ -404,14 +511,48 @@ TS_HD bool min_eig_ok(double c00, double c01, double c10, double c11) {
   return me >= -1e-9 * fmax(tr, 0.0);
 }
 
+// Solve steps of update_all for one Gaussian from its accumulated R factors (multiview.py:249-274):
+// triangulation, covariance least squares, decomposition.  Returns TS_STATUS_SOLVED /
+// TS_STATUS_UNSOLVABLE after writing the outputs, or TS_FUSE_DEFER_STATUS (outputs untouched) when
+// !allow_slow and a decision needs an SVD.
+#define TS_FUSE_DEFER_STATUS 3
+TS_HD int fuse_finish(const double *gs, const double (&R4)[4][4], const double (&R6)[6][6],
+                      const double (&c6)[6], const ts_config &cfg, double *delta, double *q,
+                      double *sc, bool allow_slow, double *dbg = nullptr) {
+  double mean[3], sol[6], qo[4], so[3];
+  int r = triangulate_from_r(R4, mean, allow_slow);
+  if (r == TS_FUSE_OK) r = cov_from_r(R6, c6, sol, allow_slow);
+  if (r == TS_FUSE_DEFER) return TS_FUSE_DEFER_STATUS;
+  bool ok = r == TS_FUSE_OK;
+  if (ok) {
+    double S[3][3] = {{sol[0], sol[1], sol[2]}, {sol[1], sol[3], sol[4]}, {sol[2], sol[4], sol[5]}};
+    if (dbg)
+      for (int i = 0; i < 6; i++) dbg[16 + i] = sol[i];
+    ok = decompose(S, gs + 3, cfg.eig_floor, qo, so, dbg);
+  }
+  ok = ok && isfinite(mean[0]) && isfinite(mean[1]) && isfinite(mean[2]) && so[0] > 0 &&
+       so[1] > 0 && so[2] > 0;
+  if (!ok) return TS_STATUS_UNSOLVABLE;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    delta[i] = mean[i] - gs[i];
+    sc[i] = so[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) q[i] = qo[i];
+  return TS_STATUS_SOLVED;
+}
+
 // update_all for one Gaussian (multiview.py:181-274).  Reads the V per-view motion records of
 // Gaussian g (stride n between views) and writes its update; returns the status.
+// With allow_slow == false the SVD-deciding Gaussians return TS_FUSE_DEFER_STATUS and leave their
+// R factors in R4 / R6 / c6 for fuse_finish in the deferred pass.
 TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera *cams, int V,
                         const ts_motions &m, const ts_config &cfg, double *delta, double *q,
-                        double *sc, double *dbg = nullptr) {
+                        double *sc, double (&R4)[4][4], double (&R6)[6][6], double (&c6)[6],
+                        bool allow_slow, double *dbg = nullptr) {
   double c3[9];
   covariance3d(gs, c3);
-  double R4[4][4], R6[6][6], c6[6];
 #pragma unroll
   for (int i = 0; i < 4; i++)
 #pragma unroll
@@ -507,26 +648,14 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     qr_add_row_rhs<6>(R6, c6, L2, mc11);
   }
   if (bad) return TS_STATUS_UNSOLVABLE;
-  double mean[3], sol[6], qo[4], so[3];
-  bool ok = triangulate_from_r(R4, mean);
-  ok = ok && cov_from_r(R6, c6, sol);
-  if (ok) {
-    double S[3][3] = {{sol[0], sol[1], sol[2]}, {sol[1], sol[3], sol[4]}, {sol[2], sol[4], sol[5]}};
-    if (dbg)
-      for (int i = 0; i < 6; i++) dbg[16 + i] = sol[i];
-    ok = decompose(S, gs + 3, cfg.eig_floor, qo, so, dbg);
-  }
-  ok = ok && isfinite(mean[0]) && isfinite(mean[1]) && isfinite(mean[2]) && so[0] > 0 &&
-       so[1] > 0 && so[2] > 0;
-  if (!ok) return TS_STATUS_UNSOLVABLE;
-#pragma unroll
-  for (int i = 0; i < 3; i++) {
-    delta[i] = mean[i] - gs[i];
-    sc[i] = so[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 4; i++) q[i] = qo[i];
-  return TS_STATUS_SOLVED;
+  return fuse_finish(gs, R4, R6, c6, cfg, delta, q, sc, allow_slow, dbg);
+}
+
+TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera *cams, int V,
+                        const ts_motions &m, const ts_config &cfg, double *delta, double *q,
+                        double *sc, double *dbg = nullptr) {
+  double R4[4][4], R6[6][6], c6[6];
+  return fuse_gaussian(gs, g, n, cams, V, m, cfg, delta, q, sc, R4, R6, c6, true, dbg);
 }
 
 }  // namespace ts
