@@ -117,6 +117,76 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
   return true;
 }
 
+// Transposed reduction of the pending Gaussians (kcount <= K2_FLUSH): lane l sums Gaussian
+// (l & 7)'s contributions over pixel quarter (l >> 3) in pixel order; two xor-shuffle steps add
+// the quarters ((q0 + q1) + (q2 + q3): commutative pairs, so all four lanes hold the same bits)
+// and the anchored moments go to the Gaussian's (instance, quadrant) sub-slot.  Warp-uniform call.
+template <typename TrackT>
+__device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params &P, int lane,
+                                         int kcount, uint32_t my_cm, uint32_t my_slot, int my_ax,
+                                         int my_ay, int qx0, int qy0) {
+  const int kk = lane & 7, qq = lane >> 3;
+  double m[TS_NMOM];
+#pragma unroll
+  for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
+  uint32_t cnt = 0, scnt = 0;
+  if (my_cm) {
+    const double ax = (double)my_ax, ay = (double)my_ay;
+    const double bx = (double)(qx0 - my_ax), by = (double)(qy0 - my_ay);
+    uint32_t bits = my_cm;
+    while (bits) {
+      const int p = __ffs(bits) - 1 + 16 * qq;
+      bits &= bits - 1;
+      const double w = S.w[kk][p];
+      const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
+      const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
+      const double wx = w * dx, wy = w * dy;
+      m[0] += w;
+      m[1] += wx;
+      m[2] += wy;
+      m[3] += wx * dx;
+      m[4] += wx * dy;
+      m[5] += wy * dy;
+      m[6] += w * ua;
+      m[7] += w * va;
+      m[8] += wx * ua;
+      m[9] += wx * va;
+      m[10] += wy * ua;
+      m[11] += wy * va;
+      if (S.trk_static[p]) {
+        m[12] += w;
+        scnt++;
+      }
+      cnt++;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < TS_NMOM; q++) {
+    m[q] += __shfl_xor_sync(0xffffffffu, m[q], 8);
+    m[q] += __shfl_xor_sync(0xffffffffu, m[q], 16);
+  }
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
+  scnt += __shfl_xor_sync(0xffffffffu, scnt, 8);
+  scnt += __shfl_xor_sync(0xffffffffu, scnt, 16);
+  if (kk < kcount && cnt > 0) {
+    // the four lanes of a Gaussian hold identical sums: each stores a quarter of the record
+    Partial *dst = P.partial + my_slot;
+    if (qq == 0) {
+      dst->m[0] = m[0]; dst->m[1] = m[1]; dst->m[2] = m[2]; dst->m[3] = m[3];
+    } else if (qq == 1) {
+      dst->m[4] = m[4]; dst->m[5] = m[5]; dst->m[6] = m[6]; dst->m[7] = m[7];
+    } else if (qq == 2) {
+      dst->m[8] = m[8]; dst->m[9] = m[9]; dst->m[10] = m[10]; dst->m[11] = m[11];
+    } else {
+      dst->m[12] = m[12];
+      dst->count = cnt;
+      dst->static_count = scnt;
+      P.flag[my_slot] = 1;
+    }
+  }
+}
+
 template <int MODE, typename TrackT>
 __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
@@ -180,6 +250,12 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
     uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
                       ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
     if (K2_STATS_ON) st[K2S_UNITS]++;
+    // pending Gaussians of the transposed reduction (accumulate mode): the lanes with
+    // (lane & 7) == k keep Gaussian k's contribution bits of their pixel quarter, its sub-slot
+    // and its anchor; a flush runs every K2_FLUSH evaluated Gaussians, across chunk boundaries
+    int kpend = 0;
+    uint32_t my_cm = 0, my_slot = 0;
+    int my_ax = 0, my_ay = 0;
     for (uint32_t b = start; b < end; b += 32) {
       if (done64 == ~0ull) break;
       if (K2_STATS_ON) {
@@ -210,12 +286,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
       uint32_t mask = __ballot_sync(0xffffffffu, hit);
       if (K2_STATS_ON) st[K2S_HITS] += __popc(mask);
       __syncwarp();
-      while (mask) {
-        // evaluate up to K2_FLUSH hitting Gaussians in depth order
-        uint32_t my_cm = 0;  // this lane's 16-pixel slice of its owned Gaussian's contributions
-        int my_j = 0;
-        int k = 0;
-        while (k < K2_FLUSH && mask) {
+      {
+        while (mask) {
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
           // warp-uniform skip of Gaussians that only cover saturated pixels
@@ -238,15 +310,27 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
                    ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
           if (MODE == K2_ACCUMULATE) {
             const bool k0 = c0 && valid0, k1 = c1 && valid1;
-            if (k0) S.w[k][lane] = w0;
-            if (k1) S.w[k][lane + 32] = w1;
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
             const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
             if (K2_STATS_ON) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
-            if ((lane & 7) == k) {
-              const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
-              my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
-              my_j = j;
+            if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
+              if (k0) S.w[kpend][lane] = w0;
+              if (k1) S.w[kpend][lane + 32] = w1;
+              if ((lane & 7) == kpend) {
+                const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
+                my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
+                my_slot = S.slot[j];
+                my_ax = anchor_x(r);
+                my_ay = anchor_y(r);
+              }
+              if (++kpend == K2_FLUSH) {
+                __syncwarp();
+                if (K2_STATS_ON) st[K2S_FLUSHES]++;
+                k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0);
+                __syncwarp();
+                kpend = 0;
+                my_cm = 0;
+              }
             }
           } else if (MODE == K2_EMIT) {
             if (c0 || c1) {
@@ -281,74 +365,14 @@ __global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) 
               best_gv1 = S.slot[j];
             }
           }
-          k++;
-        }
-        if (MODE == K2_ACCUMULATE) {
-          __syncwarp();
-          if (__any_sync(0xffffffffu, my_cm != 0)) {
-            if (K2_STATS_ON) st[K2S_FLUSHES]++;
-            // lane: Gaussian kk = lane & 7 of this flush, pixel quarter qq = lane >> 3
-            const int kk = lane & 7, qq = lane >> 3;
-            double m[TS_NMOM];
-#pragma unroll
-            for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
-            uint32_t cnt = 0, scnt = 0;
-            if (my_cm) {
-              const RasterRec &r = S.rec[my_j];
-              const int axi = anchor_x(r), ayi = anchor_y(r);
-              const double ax = (double)axi, ay = (double)ayi;
-              const double bx = (double)(qx0 - axi), by = (double)(qy0 - ayi);
-              uint32_t bits = my_cm;
-              while (bits) {
-                const int p = __ffs(bits) - 1 + 16 * qq;
-                bits &= bits - 1;
-                const double w = S.w[kk][p];
-                const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
-                const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
-                const double wx = w * dx, wy = w * dy;
-                m[0] += w;
-                m[1] += wx;
-                m[2] += wy;
-                m[3] += wx * dx;
-                m[4] += wx * dy;
-                m[5] += wy * dy;
-                m[6] += w * ua;
-                m[7] += w * va;
-                m[8] += wx * ua;
-                m[9] += wx * va;
-                m[10] += wy * ua;
-                m[11] += wy * va;
-                if (S.trk_static[p]) {
-                  m[12] += w;
-                  scnt++;
-                }
-                cnt++;
-              }
-            }
-            // add the four pixel quarters: (q0 + q1) + (q2 + q3) in every lane (commutative
-            // pairs, so all four lanes of a Gaussian hold identical bits)
-#pragma unroll
-            for (int q = 0; q < TS_NMOM; q++) {
-              m[q] += __shfl_xor_sync(0xffffffffu, m[q], 8);
-              m[q] += __shfl_xor_sync(0xffffffffu, m[q], 16);
-            }
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
-            scnt += __shfl_xor_sync(0xffffffffu, scnt, 8);
-            scnt += __shfl_xor_sync(0xffffffffu, scnt, 16);
-            if (qq == 0 && kk < k && cnt > 0) {
-              const uint32_t slot = S.slot[my_j];
-              Partial *dst = P.partial + slot;
-#pragma unroll
-              for (int q = 0; q < TS_NMOM; q++) dst->m[q] = m[q];
-              dst->count = cnt;
-              dst->static_count = scnt;
-              P.flag[slot] = 1;
-            }
-          }
-          __syncwarp();
         }
       }
+    }
+    if (MODE == K2_ACCUMULATE && kpend > 0) {
+      __syncwarp();
+      if (K2_STATS_ON) st[K2S_FLUSHES]++;
+      k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0);
+      __syncwarp();
     }
     if (MODE == K2_DOMINANT) {
       if (in0) {
