@@ -6,6 +6,8 @@
 // shapes (OpenBLAS dgemm accumulates k = 0..2 with FMA) -- pinned bit-for-bit by the oracle tests.
 #pragma once
 
+#include <cstddef>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -174,6 +176,25 @@ TS_HD int footprint(const Projection &p, double opacity, int W, int H,
   return 3;
 }
 
+// 1-based index of the lowest set bit (0 for x == 0), host and device
+TS_HD int ffs_hd(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return __ffs((int)x);
+#else
+  return __builtin_ffs((int)x);
+#endif
+}
+
+TS_HD uint64_t double_bits(double d) {
+#ifdef __CUDA_ARCH__
+  return (uint64_t)__double_as_longlong(d);
+#else
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return u;
+#endif
+}
+
 // Mahalanobis q in numpy's evaluation order (splat.py:153):
 //   ((i00*dx)*dx + ((2*i01)*dx)*dy) + (i11*dy)*dy
 TS_HD double mahalanobis(const RasterRec &r, double dx, double dy) {
@@ -232,6 +253,8 @@ struct __align__(16) Partial {
   uint64_t pad;
 };
 static_assert(sizeof(Partial) == 128, "Partial must be 128 bytes");
+static_assert(offsetof(Partial, count) == 104 && offsetof(Partial, static_count) == 108,
+              "K3 reads (count, static_count) as the second half of the 7th 16-byte vector");
 
 TS_HD int anchor_x(const RasterRec &r) { return ((int)r.x0 + (int)r.x1) >> 1; }
 TS_HD int anchor_y(const RasterRec &r) { return ((int)r.y0 + (int)r.y1) >> 1; }

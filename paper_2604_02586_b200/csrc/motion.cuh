@@ -96,13 +96,28 @@ TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t ba
 #pragma unroll
   for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
   uint32_t cnt = 0, scnt = 0;
-  for (uint32_t i = 0; i < nslots; i++) {
-    if (!flag[base4 + i]) continue;
-    const Partial &p = partial[base4 + i];
+  // nslots is a multiple of TS_K2_SUBS = 4 and base4 is 4-aligned: one 32-bit word holds the
+  // flags of an instance's four quadrant sub-slots; records are read as 16-byte vectors
+  static_assert(TS_K2_SUBS == 4, "flag words assume four sub-slots per instance");
+  for (uint32_t i = 0; i < nslots; i += 4) {
+    uint32_t f4 = *reinterpret_cast<const uint32_t *>(flag + base4 + i);
+    while (f4) {
+      const int sub = (ffs_hd(f4) - 1) >> 3;
+      f4 &= ~(0xFFu << (8 * sub));
+      const double2 *p2 = reinterpret_cast<const double2 *>(partial + base4 + i + sub);
+      double2 v[7];  // m[0..12] and (count, static_count) in the low / high words of v[6].y
 #pragma unroll
-    for (int k = 0; k < TS_NMOM; k++) mom[k] += p.m[k];
-    cnt += p.count;
-    scnt += p.static_count;
+      for (int k = 0; k < 7; k++) v[k] = p2[k];
+#pragma unroll
+      for (int k = 0; k < 6; k++) {
+        mom[2 * k] += v[k].x;
+        mom[2 * k + 1] += v[k].y;
+      }
+      mom[12] += v[6].x;
+      const uint64_t counts = double_bits(v[6].y);
+      cnt += (uint32_t)counts;
+      scnt += (uint32_t)(counts >> 32);
+    }
   }
   GvMotion r;
   r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;

@@ -25,7 +25,10 @@ __device__ __forceinline__ bool finite6(const double *x) {
   return ok;
 }
 
-__global__ void __launch_bounds__(256) k3_solve(const Partial *__restrict__ partial,
+#ifndef TS_K3_MIN_BLOCKS
+#define TS_K3_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial *__restrict__ partial,
                                                 const uint8_t *__restrict__ flag,
                                                 const uint32_t *__restrict__ inst_base,
                                                 const uint32_t *__restrict__ ntiles,
