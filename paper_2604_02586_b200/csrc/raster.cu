@@ -27,7 +27,13 @@
 namespace ts {
 
 constexpr int K2_WARPS = 4;     // warps per CTA (independent; shared memory partitioned)
-constexpr int K2_FLUSH = 8;     // evaluated Gaussians per transposed reduction
+#ifndef TS_K2_FLUSH
+#define TS_K2_FLUSH 8
+#endif
+#ifndef TS_K2_MIN_BLOCKS
+#define TS_K2_MIN_BLOCKS 6
+#endif
+constexpr int K2_FLUSH = TS_K2_FLUSH;  // evaluated Gaussians per transposed reduction
 constexpr int K2_WROW = 65;     // padded row of the w buffer (64 pixels)
 constexpr int K2_ETAB_BYTES = ((TS_EXP_TABLE * 8 + 127) / 128) * 128;
 
@@ -188,7 +194,7 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
 }
 
 template <int MODE, typename TrackT>
-__global__ void __launch_bounds__(K2_WARPS * 32, 6) k2_raster(const K2Params P) {
+__global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
   double *etab = reinterpret_cast<double *>(k2_smem_raw);  // exp(-k/64), k = 0..288
   for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
