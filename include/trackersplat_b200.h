@@ -123,9 +123,11 @@ int ts_frame_compensate(ts_plan *plan, const void *track_target, int32_t track_d
 typedef struct ts_binning {
   int64_t n_instances;
   int32_t tiles_x, tiles_y, n_views;
-  const uint32_t *inst_tile; /* (n_instances) sorted global tile ids               */
-  const uint32_t *inst_gv;   /* (n_instances) gv of each instance, (depth, g) order */
-  const uint32_t *tile_range;/* (V*tiles, 2) [start, end) into the instance arrays  */
+  const uint32_t *inst_tile; /* (n_instances) tile id within the view; instances are
+                                grouped by tile position, views in order            */
+  const uint32_t *inst_gv;   /* (n_instances) gv = v*N + g; each (view, tile) list in
+                                the reference's (depth, g) order                    */
+  const uint32_t *tile_range;/* (V*tiles, 2) [start, end) of global tile v*tiles + t */
   const int8_t *gv_status;   /* (V*N) 0 behind, 1 degenerate, 2 empty bbox, 3 binned */
   const int16_t *gv_bbox;    /* (V*N, 4) x0 x1 y0 y1                                 */
 } ts_binning;

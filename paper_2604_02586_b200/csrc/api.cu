@@ -285,13 +285,14 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
     launch_k1_emit(ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->cnt_sorted), ptr<uint32_t>(p->off_sorted),
                    ptr<RasterRec>(p->rec), NV, n, p->tiles_x, p->tpv, ptr<uint32_t>(p->tkey),
                    ptr<uint32_t>(p->tval), s);
-    const int tbits = bits_for((uint64_t)ntile_total);
+    const int tbits = bits_for((uint64_t)p->tpv);  // tile within the view (see binning.cu)
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
       return cub::DeviceRadixSort::SortPairs(tmp, bytes, ptr<uint32_t>(p->tkey),
                                              ptr<uint32_t>(p->tkey2), ptr<uint32_t>(p->tval),
                                              ptr<uint32_t>(p->tval2), (int)ni, 0, tbits, s);
     }));
-    launch_k1_tile_ranges(ptr<uint32_t>(p->tkey2), ni, ptr<uint32_t>(p->range), s);
+    launch_k1_tile_ranges(ptr<uint32_t>(p->tkey2), ptr<uint32_t>(p->tval2), ni, n, p->tpv,
+                          ptr<uint32_t>(p->range), s);
   }
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_TILE_SORT, e2, s);

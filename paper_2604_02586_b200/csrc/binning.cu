@@ -10,9 +10,12 @@
 //   2. CUB radix sort by that key (31 bits at V=20, 4 passes).  Rounding to f32 and dropping low
 //      mantissa bits are monotone, so the order is right except inside runs of equal keys;
 //      k1_fix_ties re-sorts those (short) runs by the exact (f64 depth, gid) key.
-//   3. k1_emit writes one (tile, gv) instance per covered tile in that depth order; a stable CUB
-//      radix sort on the tile id alone then yields tile-major, depth-ordered lists.
-//   4. k1_tile_ranges marks [start, end) of every tile.
+//   3. k1_emit writes one (tile, gv) instance per covered tile in that depth order (views are
+//      contiguous: the view is the top field of the depth key); a stable CUB radix sort on the
+//      tile id WITHIN the view (13 bits at 1352x1014: two onesweep passes instead of three for
+//      the global id) then groups every tile position tile-major, views in order, each
+//      (view, tile) list depth-ordered.
+//   4. k1_tile_ranges marks [start, end) of every (view, tile).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -110,22 +113,27 @@ __global__ void k1_emit(const uint32_t *__restrict__ val, const uint32_t *__rest
   uint32_t v = (uint32_t)(gv / n);
   RasterRec r = rec[gv];
   uint32_t o = off_sorted[k];
-  uint32_t base = v * (uint32_t)tiles_per_view;
+  (void)v;
   for (int ty = r.y0 / TS_TILE; ty <= r.y1 / TS_TILE; ty++)
     for (int tx = r.x0 / TS_TILE; tx <= r.x1 / TS_TILE; tx++) {
-      tkey[o] = base + (uint32_t)(ty * tiles_x + tx);
+      tkey[o] = (uint32_t)(ty * tiles_x + tx);  // tile within the view
       tval[o] = gv;
       o++;
     }
 }
 
-__global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, int64_t n_inst,
+__global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, const uint32_t *__restrict__ tval,
+                               int64_t n_inst, int64_t n, int tiles_per_view,
                                uint32_t *__restrict__ range) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_inst) return;
-  uint32_t t = tkey[i];
-  if (i == 0 || tkey[i - 1] != t) range[2 * t] = (uint32_t)i;
-  if (i == n_inst - 1 || tkey[i + 1] != t) range[2 * t + 1] = (uint32_t)(i + 1);
+  // global tile id = view * tiles_per_view + tile-in-view; runs are contiguous after the sort
+  const uint32_t t = (uint32_t)(tval[i] / n) * (uint32_t)tiles_per_view + tkey[i];
+  const bool first = i == 0 || (uint32_t)(tval[i - 1] / n) * (uint32_t)tiles_per_view + tkey[i - 1] != t;
+  const bool last = i == n_inst - 1 ||
+                    (uint32_t)(tval[i + 1] / n) * (uint32_t)tiles_per_view + tkey[i + 1] != t;
+  if (first) range[2 * t] = (uint32_t)i;
+  if (last) range[2 * t + 1] = (uint32_t)(i + 1);
 }
 
 // _project_all for the stage API (one view).
@@ -174,8 +182,10 @@ void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint3
     k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, cnt_sorted, off_sorted, rec, M, n, tiles_x,
                                            tiles_per_view, tkey, tval);
 }
-void launch_k1_tile_ranges(const uint32_t *tkey, int64_t n_inst, uint32_t *range, cudaStream_t s) {
-  if (n_inst) k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, n_inst, range);
+void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
+                           int tiles_per_view, uint32_t *range, cudaStream_t s) {
+  if (n_inst)
+    k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, tval, n_inst, n, tiles_per_view, range);
 }
 void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
                          double *depth, double *cov2, uint8_t *in_front, cudaStream_t s) {

@@ -32,3 +32,15 @@ def weightmap(d, prefix):
 def motions(d):
     return dict(status=d["m_status"], a=d["m_a"], b=d["m_b"], weight_sum=d["m_w"],
                 pixel_count=d["m_cnt"])
+
+
+def tile_order_index(ranges):
+    """Instance indices of one view's tiles in tile order, from its (tiles, 2) [start, end)
+    ranges (empty tiles contribute nothing)."""
+    ranges = np.asarray(ranges, np.int64)
+    cnt = ranges[:, 1] - ranges[:, 0]
+    if not cnt.any():
+        return np.zeros(0, np.int64)
+    starts = np.repeat(ranges[:, 0], cnt)
+    within = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    return starts + within
