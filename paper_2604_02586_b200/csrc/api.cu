@@ -66,7 +66,7 @@ struct ts_plan {
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
   // regularisation buffers
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
-      reg_static, reg_source, reg_euler, k4_ws;
+      reg_static, reg_source, reg_euler, k4_ws, drange;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
   int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
@@ -120,7 +120,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end,
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
-                          &p->reg_source, &p->reg_euler, &p->k4_ws};
+                          &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -137,7 +137,7 @@ void release_all(ts_plan *p) {
                     &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
-                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws};
+                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -237,7 +237,9 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->counters, 64);
 
   cudaEvent_t e0 = p->mark_begin(s);
-  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->dkey),
+  ENSURE(p->drange, 8 * 64);
+  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec),
+                    ptr<uint32_t>(p->drange), ptr<uint32_t>(p->dkey),
                     ptr<uint32_t>(p->dval), ptr<double>(p->depth64), ptr<uint32_t>(p->ntiles),
                     ptr<int8_t>(p->status), ptr<int16_t>(p->bbox), s);
   TS_CUDA_TRY(cudaGetLastError());

@@ -24,7 +24,7 @@ namespace ts {
 __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, int64_t n,
                                                   const ts_camera *__restrict__ cams, int V,
                                                   RasterRec *__restrict__ rec,
-                                                  uint32_t *__restrict__ dkey,
+                                                  uint32_t *__restrict__ drange,
                                                   uint32_t *__restrict__ dval,
                                                   double *__restrict__ depth64,
                                                   uint32_t *__restrict__ ntiles,
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, 
   extern __shared__ ts_camera s_cam[];
   for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam[i] = cams[i];
   __syncthreads();
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   double gs[11];
 #pragma unroll
@@ -47,26 +47,72 @@ __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, 
     RasterRec r;
     int st = footprint(p, gs[10], cam.width, cam.height, r);
     int64_t gv = (int64_t)v * n + g;
-    status[gv] = (int8_t)st;
-    uint32_t key = ((uint32_t)v << 26);
     uint32_t nt = 0;
     int16_t bb[4] = {0, -1, 0, -1};
+    status[gv] = (int8_t)st;
     if (st == 3) {
       r.g = (uint32_t)g;
       r.pad = 0;
       rec[gv] = r;
-      key |= __float_as_uint(__double2float_rn(p.depth)) >> 5;  // depth > 0: < 0x3FC0000
-      nt = (uint32_t)((r.x1 / TS_TILE - r.x0 / TS_TILE + 1) * (r.y1 / TS_TILE - r.y0 / TS_TILE + 1));
+      nt = (uint32_t)((r.x1 / TS_TILE - r.x0 / TS_TILE + 1) *
+                      (r.y1 / TS_TILE - r.y0 / TS_TILE + 1));
       bb[0] = r.x0; bb[1] = r.x1; bb[2] = r.y0; bb[3] = r.y1;
-    } else {
-      key |= 0x3FFFFFFu;  // sorts after every binned Gaussian of the view, never emitted
     }
-    dkey[gv] = key;
     dval[gv] = (uint32_t)gv;
-    depth64[gv] = p.depth;
+    depth64[gv] = st == 3 ? p.depth : -1.0;  // -1: not binned (excluded from the depth range)
     ntiles[gv] = nt;
     reinterpret_cast<short4 *>(bbox)[gv] = make_short4(bb[0], bb[1], bb[2], bb[3]);
   }
+}
+
+// Per-view range of the binned depths (float bits, widened by directed rounding so that every
+// double depth lies inside; depth > 1e-6 > 0, so positive-float bit order is numeric order).
+__global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__ depth64,
+                                                      int64_t n, uint32_t *__restrict__ drange) {
+  const int v = blockIdx.y;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const double d = depth64[(int64_t)v * n + g];
+    if (d > 0.0) {
+      lo = min(lo, __float_as_uint(__double2float_rd(d)));
+      hi = max(hi, __float_as_uint(__double2float_ru(d)));
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lo != 0xFFFFFFFFu) atomicMin(&drange[2 * v], lo);
+    if (hi != 0u) atomicMax(&drange[2 * v + 1], hi);
+  }
+}
+
+// 32-bit depth keys v << 26 | q, q = floor((d - dmin) * (2^26 - 2) / (dmax - dmin)) over the
+// view's depth range: monotone in d (so the radix sort plus the exact tie repair below yields
+// the reference's (depth, gid) order) and resolving ~2^26 levels per view instead of the 18
+// mantissa bits a truncated float key keeps (far fewer ties to repair).
+__global__ void k1_depth_keys(const double *__restrict__ depth64,
+                              const int8_t *__restrict__ status,
+                              const uint32_t *__restrict__ drange, int64_t n, int V,
+                              uint32_t *__restrict__ dkey) {
+  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gv >= n * V) return;
+  const uint32_t v = (uint32_t)(gv / n);
+  uint32_t key = v << 26;
+  if (status[gv] == 3) {
+    const double dmin = (double)__uint_as_float(drange[2 * v]);
+    const double dmax = (double)__uint_as_float(drange[2 * v + 1]);
+    const double span = dmax - dmin;
+    const double scale = span > 0.0 ? 67108862.0 / span : 0.0;
+    const double qd = fmin(fmax((depth64[gv] - dmin) * scale, 0.0), 67108862.0);
+    key |= (uint32_t)qd;
+  } else {
+    key |= 0x3FFFFFFu;  // sorts after every binned Gaussian of the view, never emitted
+  }
+  dkey[gv] = key;
 }
 
 // Re-sort runs of equal (view, f32 depth) keys by the exact (f64 depth, gid) key.
@@ -101,25 +147,55 @@ __global__ void k1_gather_counts(const uint32_t *__restrict__ val, const uint32_
   if (k < M) cnt_sorted[k] = ntiles[val[k]];
 }
 
-__global__ void k1_emit(const uint32_t *__restrict__ val, const uint32_t *__restrict__ cnt_sorted,
-                        const uint32_t *__restrict__ off_sorted, const RasterRec *__restrict__ rec,
-                        int64_t M, int64_t n, int tiles_x, int tiles_per_view,
-                        uint32_t *__restrict__ tkey, uint32_t *__restrict__ tval) {
-  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= M) return;
-  uint32_t c = cnt_sorted[k];
-  if (c == 0) return;
-  uint32_t gv = val[k];
-  uint32_t v = (uint32_t)(gv / n);
-  RasterRec r = rec[gv];
-  uint32_t o = off_sorted[k];
-  (void)v;
-  for (int ty = r.y0 / TS_TILE; ty <= r.y1 / TS_TILE; ty++)
-    for (int tx = r.x0 / TS_TILE; tx <= r.x1 / TS_TILE; tx++) {
-      tkey[o] = (uint32_t)(ty * tiles_x + tx);  // tile within the view
-      tval[o] = gv;
-      o++;
+// One warp per 32 consecutive depth-sorted gvs: their instances are one contiguous run of the
+// output (exclusive scan of the counts), so the lanes write it cooperatively -- instance e of the
+// run belongs to the last lane whose offset is <= e (binary search over the 32 offsets) and is
+// its (k / width, k % width) tile, k = e - offset.  Coalesced stores and no per-lane loop over
+// large bounding boxes (a 200-tile Gaussian no longer idles 31 lanes).
+__global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
+                                               const uint32_t *__restrict__ cnt_sorted,
+                                               const uint32_t *__restrict__ off_sorted,
+                                               const RasterRec *__restrict__ rec, int64_t M,
+                                               int tiles_x, uint32_t *__restrict__ tkey,
+                                               uint32_t *__restrict__ tval) {
+  struct Owner {
+    uint32_t off, gv;
+    int16_t tx0, ty0, wt, pad;
+  };
+  __shared__ Owner s_own[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  uint32_t c = 0, o;
+  Owner me{0u, 0u, 0, 0, 1, 0};
+  if (k < M) {
+    c = cnt_sorted[k];
+    o = off_sorted[k];
+    if (c) {
+      me.gv = val[k];
+      const RasterRec r = rec[me.gv];
+      me.tx0 = (int16_t)(r.x0 / TS_TILE);
+      me.ty0 = (int16_t)(r.y0 / TS_TILE);
+      me.wt = (int16_t)(r.x1 / TS_TILE - me.tx0 + 1);
     }
+  } else {
+    o = off_sorted[M - 1] + cnt_sorted[M - 1];  // past the end: offset = total
+  }
+  const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
+  const uint32_t end = __shfl_sync(0xffffffffu, o + c, 31);
+  me.off = o - base;  // non-decreasing over the lanes; empty lanes repeat the next offset
+  s_own[w][lane] = me;
+  __syncwarp();
+  for (uint32_t e = lane; e < end - base; e += 32) {
+    int j = 0;  // last lane with off <= e: it owns instance e (empty lanes precede equal offsets)
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (s_own[w][j + step].off <= e) j += step;
+    const Owner ow = s_own[w][j];
+    const uint32_t kk = e - ow.off;
+    const int ty = ow.ty0 + (int)(kk / (uint32_t)ow.wt), tx = ow.tx0 + (int)(kk % (uint32_t)ow.wt);
+    tkey[base + e] = (uint32_t)(ty * tiles_x + tx);  // tile within the view
+    tval[base + e] = ow.gv;
+  }
 }
 
 __global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, const uint32_t *__restrict__ tval,
@@ -160,12 +236,23 @@ __global__ void k_project_view(const double *__restrict__ G, int64_t n, ts_camer
 
 static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+__global__ void k1_range_init(uint32_t *drange, int V) {
+  const int i = threadIdx.x;
+  if (i < V) {
+    drange[2 * i] = 0xFFFFFFFFu;
+    drange[2 * i + 1] = 0u;
+  }
+}
+
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint32_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
-                       int8_t *status, int16_t *bbox, cudaStream_t s) {
+                       uint32_t *drange, uint32_t *dkey, uint32_t *dval, double *depth64,
+                       uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s) {
   if (n == 0) return;
-  k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, dkey, dval,
+  k1_range_init<<<1, 64, 0, s>>>(drange, V);
+  k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, drange, dval,
                                                                   depth64, ntiles, status, bbox);
+  k1_depth_range<<<dim3(16, V), 256, 0, s>>>(depth64, n, drange);
+  k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dkey);
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         cudaStream_t s) {
@@ -179,8 +266,8 @@ void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint3
                     const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
                     uint32_t *tkey, uint32_t *tval, cudaStream_t s) {
   if (M)
-    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, cnt_sorted, off_sorted, rec, M, n, tiles_x,
-                                           tiles_per_view, tkey, tval);
+    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, cnt_sorted, off_sorted, rec, M, tiles_x, tkey,
+                                           tval);
 }
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
                            int tiles_per_view, uint32_t *range, cudaStream_t s) {

@@ -8,8 +8,8 @@ namespace ts {
 enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
 
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint32_t *dkey, uint32_t *dval, double *depth64, uint32_t *ntiles,
-                       int8_t *status, int16_t *bbox, cudaStream_t s);
+                       uint32_t *drange, uint32_t *dkey, uint32_t *dval, double *depth64,
+                       uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s);
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         cudaStream_t s);
 void launch_k1_gather_counts(const uint32_t *val, const uint32_t *ntiles, uint32_t *cnt_sorted,
