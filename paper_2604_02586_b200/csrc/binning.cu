@@ -199,17 +199,19 @@ __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
 }
 
 __global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, const uint32_t *__restrict__ tval,
-                               int64_t n_inst, int64_t n, int tiles_per_view,
+                               int64_t n_inst, double inv_n, int tiles_per_view,
                                uint32_t *__restrict__ range) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_inst) return;
-  // global tile id = view * tiles_per_view + tile-in-view; runs are contiguous after the sort
-  const uint32_t t = (uint32_t)(tval[i] / n) * (uint32_t)tiles_per_view + tkey[i];
-  const bool first = i == 0 || (uint32_t)(tval[i - 1] / n) * (uint32_t)tiles_per_view + tkey[i - 1] != t;
-  const bool last = i == n_inst - 1 ||
-                    (uint32_t)(tval[i + 1] / n) * (uint32_t)tiles_per_view + tkey[i + 1] != t;
-  if (first) range[2 * t] = (uint32_t)i;
-  if (last) range[2 * t + 1] = (uint32_t)(i + 1);
+  // global tile id = view * tiles_per_view + tile-in-view, view = gv / n computed as
+  // floor((gv + 0.5) / n) in fp64 (exact: the quotient is never within 2e-10 of an integer)
+  auto gtile = [&](int64_t k) {
+    const uint32_t v = (uint32_t)(((double)tval[k] + 0.5) * inv_n);
+    return v * (uint32_t)tiles_per_view + tkey[k];
+  };
+  const uint32_t t = gtile(i);
+  if (i == 0 || gtile(i - 1) != t) range[2 * t] = (uint32_t)i;
+  if (i == n_inst - 1 || gtile(i + 1) != t) range[2 * t + 1] = (uint32_t)(i + 1);
 }
 
 // _project_all for the stage API (one view).
@@ -272,7 +274,8 @@ void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint3
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
                            int tiles_per_view, uint32_t *range, cudaStream_t s) {
   if (n_inst)
-    k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, tval, n_inst, n, tiles_per_view, range);
+    k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, tval, n_inst, 1.0 / (double)n,
+                                                       tiles_per_view, range);
 }
 void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
                          double *depth, double *cov2, uint8_t *in_front, cudaStream_t s) {
