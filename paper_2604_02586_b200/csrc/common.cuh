@@ -185,6 +185,14 @@ TS_HD int ffs_hd(uint32_t x) {
 #endif
 }
 
+TS_HD int ffs64_hd(uint64_t x) {
+#ifdef __CUDA_ARCH__
+  return __ffsll((long long)x);
+#else
+  return __builtin_ffsll((long long)x);
+#endif
+}
+
 TS_HD uint64_t double_bits(double d) {
 #ifdef __CUDA_ARCH__
   return (uint64_t)__double_as_longlong(d);

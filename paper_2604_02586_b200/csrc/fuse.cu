@@ -20,6 +20,8 @@
 
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "smallsolve.cuh"
 
 namespace ts {
@@ -49,15 +51,52 @@ __device__ __forceinline__ void store_updates(ts_updates u, int64_t g, const dou
 #ifndef TS_K4_MIN_BLOCKS
 #define TS_K4_MIN_BLOCKS 3
 #endif
+// Eligibility pre-pass of update_all (multiview.py:231-235): ineligible Gaussians get their
+// UNSOLVABLE update here; eligible ones are keyed by their solved-view count so that a radix sort
+// groups Gaussians of equal work into the same warps of k4_fuse (the streaming QR loops over the
+// solved views: mixed counts and early exits left ~12 of 32 lanes active).
+__global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int64_t n, int V,
+                                               ts_motions m, ts_config cfg, ts_updates u,
+                                               uint32_t *__restrict__ key,
+                                               uint32_t *__restrict__ val) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  int n_solved = 0;
+  double tw = 0.0;
+  int64_t tp = 0;
+  for (int v = 0; v < V; v++) {
+    const int64_t gv = (int64_t)v * n + g;
+    if (m.status[gv] != TS_STATUS_SOLVED) continue;
+    n_solved++;
+    tw += m.weight_sum[gv];
+    tp += m.pixel_count[gv];
+  }
+  const bool ok = n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
+                  tp >= cfg.min_total_pixels;
+  key[g] = ok ? (uint32_t)n_solved : 0xFFu;
+  val[g] = (uint32_t)g;
+  if (!ok) {
+    double delta[3] = {0.0, 0.0, 0.0}, q[4], sc[3];
+#pragma unroll
+    for (int i = 0; i < 4; i++) q[i] = G[11 * g + 3 + i];
+#pragma unroll
+    for (int i = 0; i < 3; i++) sc[i] = G[11 * g + 7 + i];
+    store_updates(u, g, delta, q, sc, TS_STATUS_UNSOLVABLE);
+  }
+}
+
 __global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *__restrict__ G, int64_t n,
                                                const ts_camera *__restrict__ cams, int V,
                                                ts_motions m, ts_config cfg, ts_updates u,
+                                               const uint32_t *__restrict__ order_key,
+                                               const uint32_t *__restrict__ order,
                                                K4Deferred *defer, unsigned *n_defer) {
   extern __shared__ ts_camera s_cam4[];
   for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam4[i] = cams[i];
   __syncthreads();
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || order_key[t] == 0xFFu) return;  // ineligible: written by k4_prep
+  const int64_t g = order[t];
   double gs[11];
 #pragma unroll
   for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
@@ -205,16 +244,35 @@ void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, t
                      const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s) {
   k4_debug<<<1, 1, 0, s>>>(G, n, cams, V, m, cfg, g, dbg);
 }
-size_t k4_workspace_bytes(int64_t n) { return 256 + sizeof(K4Deferred) * (size_t)n; }
+// workspace: [counter | deferred records | 4 key/value arrays | CUB temp]
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+static size_t k4_sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n, 0, 8);
+  return bytes;
+}
+size_t k4_workspace_bytes(int64_t n) {
+  return 256 + align256(sizeof(K4Deferred) * (size_t)n) + 4 * align256(4 * (size_t)n) +
+         align256(k4_sort_temp_bytes(n));
+}
 
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
                     const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s) {
   if (!n) return;
-  unsigned *n_defer = reinterpret_cast<unsigned *>(workspace);
-  K4Deferred *defer = reinterpret_cast<K4Deferred *>(reinterpret_cast<char *>(workspace) + 256);
+  char *ws = reinterpret_cast<char *>(workspace);
+  unsigned *n_defer = reinterpret_cast<unsigned *>(ws);
+  K4Deferred *defer = reinterpret_cast<K4Deferred *>(ws + 256);
+  char *kv = ws + 256 + align256(sizeof(K4Deferred) * (size_t)n);
+  uint32_t *key = reinterpret_cast<uint32_t *>(kv), *val = key + align256(4 * (size_t)n) / 4;
+  uint32_t *key2 = val + align256(4 * (size_t)n) / 4, *val2 = key2 + align256(4 * (size_t)n) / 4;
+  void *tmp = val2 + align256(4 * (size_t)n) / 4;
+  size_t tmp_bytes = k4_sort_temp_bytes(n);
   cudaMemsetAsync(n_defer, 0, sizeof(unsigned), s);
-  k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u, defer,
-                                                              n_defer);
+  k4_prep<<<blocks(n, 256), 256, 0, s>>>(G, n, V, m, cfg, u, key, val);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, val, val2, (int)n, 0, 8, s);
+  k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u, key2, val2,
+                                                              defer, n_defer);
   const unsigned fin_blocks = (unsigned)std::min<int64_t>(blocks(n, 128), 148 * 4);
   k4_finish<<<fin_blocks, 128, 0, s>>>(G, cfg, u, defer, n_defer);
 }

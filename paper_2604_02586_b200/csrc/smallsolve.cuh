@@ -568,9 +568,11 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   int n_solved = 0;
   double tw = 0.0;
   int64_t tp = 0;
+  uint64_t solved = 0;  // bit v: view v SOLVED (V <= 64)
   for (int v = 0; v < V; v++) {
     const int64_t gv = (int64_t)v * n + g;
     if (m.status[gv] != TS_STATUS_SOLVED) continue;
+    solved |= 1ull << v;
     n_solved++;
     tw += m.weight_sum[gv];
     tp += m.pixel_count[gv];
@@ -585,9 +587,12 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   if (!(n_solved >= cfg.min_views && tw >= cfg.min_total_weight && tp >= cfg.min_total_pixels))
     return TS_STATUS_UNSOLVABLE;
   bool bad = false;
-  for (int v = 0; v < V && !bad; v++) {
+  // iterate the solved views only, in view order: Gaussians with equal solved-view counts (k4_fuse
+  // groups them) then run the heavy body in lockstep
+  while (solved && !bad) {
+    const int v = ffs64_hd(solved) - 1;
+    solved &= solved - 1;
     const int64_t gv = (int64_t)v * n + g;
-    if (m.status[gv] != TS_STATUS_SOLVED) continue;
     const ts_camera &cam = cams[v];
     Projection p;
     project(gs, c3, cam, p);
