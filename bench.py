@@ -53,7 +53,7 @@ CONFIGS = {
 METRIC = "Gaussian-views/sec motion-fit"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
-LAUNCHES_PER_STEP = 25  # our kernels per frame incl. CUB passes (profiles/r01_launches_cfg2.txt)
+LAUNCHES_PER_STEP = 31  # our kernels per frame incl. CUB passes (profiles/r01_launches_cfg2.txt: 62 per 2 frames)
 
 
 def log(*a):
