@@ -179,10 +179,14 @@ class FrameEngine:
 class StreamingEngine:
     """Double-buffered end-to-end driver: pinned host inputs in, pinned host results out.
 
-    Every step copies its own inputs (Gaussians + tracks) host->device and reads its result back
-    device->host; the copies of step k+1 run on a copy stream while step k computes on the
-    compute stream (two input slots, ordered with CUDA events).  This is how a caller streams the
-    target frames of a clip through the hot path.
+    Three streams: H2D copies, compute, D2H copies.  `step(inputs_k)` enqueues the H2D copy of
+    inputs k and then the compute of the PREVIOUS step (k-1), so the copy of step k is already
+    queued when step k-1's binning briefly synchronises the host (the instance count); the D2H of
+    a step's results runs on its own stream from one of two output buffers, so the compute stream
+    moves on to the next frame at once.  The PCIe transfers of the next frame therefore overlap
+    the whole compute of the current one.  Input slots and output buffers are reused in turn,
+    ordered with CUDA events.  `step` returns the event after which the previous step's results
+    are in its host buffer (None for the first call); `flush()` runs the last pending step.
     """
 
     def __init__(self, engine: FrameEngine | None = None):
@@ -190,10 +194,14 @@ class StreamingEngine:
         self.eng = engine if engine is not None else FrameEngine()
         self.copy_stream = torch.cuda.Stream()
         self.comp_stream = torch.cuda.Stream()
+        self.d2h_stream = torch.cuda.Stream()
         self._slots = [None, None]
-        self._free = [None, None]
+        self._free = [None, None]      # input slot i reusable after this compute event
+        self._outs = [None, None]
+        self._out_free = [None, None]  # output buffer j reusable after this D2H event
         self._k = 0
-        self.out = None
+        self._j = 0
+        self._pending = None
 
     def _slot(self, i, g_host, t_host, v_host):
         torch = _torch()
@@ -213,8 +221,37 @@ class StreamingEngine:
         torch = _torch()
         return torch.empty((n, 11), dtype=torch.float64).pin_memory()
 
+    def _compute(self, pending):
+        torch = _torch()
+        i, g_d, t_d, v_d, ready, cameras, res_host, config = pending
+        j = self._j
+        self._j ^= 1
+        cs = self.comp_stream
+        cs.wait_event(ready)
+        if self._out_free[j] is not None:
+            cs.wait_event(self._out_free[j])
+        self.eng.bin(g_d, cameras, config, stream=cs)
+        out = self.eng.compensate(t_d, v_d, self._outs[j], stream=cs)
+        self._outs[j] = out
+        with torch.cuda.stream(cs):
+            res = torch.cat([out.delta_mean, out.rotation, out.scale,
+                             out.status.to(torch.float64)[:, None]], 1)
+            computed = torch.cuda.Event()
+            computed.record(cs)
+        self._free[i] = computed
+        ds = self.d2h_stream
+        ds.wait_event(computed)
+        with torch.cuda.stream(ds):
+            res.record_stream(ds)
+            res_host.copy_(res, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(ds)
+        self._out_free[j] = done
+        self.out = out
+        return done
+
     def step(self, g_host, cameras, t_host, v_host, res_host, config=None):
-        """Enqueue one frame: H2D inputs, K1..K4, D2H result.  Returns the completion event."""
+        """Enqueue the H2D copy of this step's inputs, then compute the previous step."""
         torch = _torch()
         i = self._k % 2
         self._k += 1
@@ -227,16 +264,10 @@ class StreamingEngine:
             v_d.copy_(v_host, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self.copy_stream)
-        cs = self.comp_stream
-        cs.wait_event(ready)
-        self.eng.bin(g_d, cameras, config, stream=cs)
-        self.out = self.eng.compensate(t_d, v_d, self.out, stream=cs)
-        with torch.cuda.stream(cs):
-            o = self.out
-            res = torch.cat([o.delta_mean, o.rotation, o.scale,
-                             o.status.to(torch.float64)[:, None]], 1)
-            res_host.copy_(res, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(cs)
-        self._free[i] = done
-        return done
+        prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config)
+        return self._compute(prev) if prev is not None else None
+
+    def flush(self):
+        """Compute the last pending step; returns its results-ready event (or None)."""
+        prev, self._pending = self._pending, None
+        return self._compute(prev) if prev is not None else None

@@ -1,0 +1,43 @@
+"""StreamingEngine (engine.py): the double-buffered host-in/host-out driver returns, for every
+step, exactly what FrameEngine computes on the same inputs (the copy of step k is queued before
+step k-1's compute, so results arrive one call late; flush() drains the last one)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from tests import golden_data as gd  # noqa: E402
+
+
+def test_streaming_matches_direct():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_02586_b200.engine import FrameEngine, StreamingEngine
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    g = np.ascontiguousarray(d["gaussians"])
+    cams = d["cameras"]
+    inputs = []
+    for shift in (0.0, 0.75, -0.4, 0.0):
+        t = (target + np.array([shift, -0.5 * shift])).astype(np.float32)
+        inputs.append((torch.from_numpy(g).pin_memory(), torch.from_numpy(t).pin_memory(),
+                       torch.from_numpy(valid.astype(np.uint8)).pin_memory()))
+    streamer = StreamingEngine()
+    results = [StreamingEngine.result_buffer(len(g)) for _ in inputs]
+    events = [streamer.step(gh, cams, th, vh, res) for (gh, th, vh), res in zip(inputs, results)]
+    assert events[0] is None and all(e is not None for e in events[1:])
+    streamer.flush()
+    torch.cuda.synchronize()
+    direct = FrameEngine()
+    for (gh, th, vh), res in zip(inputs, results):
+        direct.bin(gh.numpy(), cams)
+        o = direct.compensate(th.numpy(), vh.numpy())
+        ref = torch.cat([o.delta_mean, o.rotation, o.scale,
+                         o.status.to(torch.float64)[:, None]], 1).cpu()
+        torch.testing.assert_close(res, ref, rtol=0, atol=0)
+    # the shifted inputs really produce different results
+    assert not torch.equal(results[0], results[1])
+    assert torch.equal(results[0], results[3])
