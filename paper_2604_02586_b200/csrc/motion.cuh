@@ -99,8 +99,17 @@ TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t ba
   // nslots is a multiple of TS_K2_SUBS = 4 and base4 is 4-aligned: one 32-bit word holds the
   // flags of an instance's four quadrant sub-slots; records are read as 16-byte vectors
   static_assert(TS_K2_SUBS == 4, "flag words assume four sub-slots per instance");
-  for (uint32_t i = 0; i < nslots; i += 4) {
-    uint32_t f4 = *reinterpret_cast<const uint32_t *>(flag + base4 + i);
+  for (uint32_t i0 = 0; i0 < nslots; i0 += 16) {
+    // four instances' flag words per round: independent loads in flight for large bboxes
+    uint32_t fw[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      fw[q] = i0 + 4 * q < nslots
+                  ? *reinterpret_cast<const uint32_t *>(flag + base4 + i0 + 4 * q) : 0u;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+    const uint32_t i = i0 + 4 * q;
+    uint32_t f4 = fw[q];
     while (f4) {
       const int sub = (ffs_hd(f4) - 1) >> 3;
       f4 &= ~(0xFFu << (8 * sub));
@@ -117,6 +126,7 @@ TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t ba
       const uint64_t counts = double_bits(v[6].y);
       cnt += (uint32_t)counts;
       scnt += (uint32_t)(counts >> 32);
+    }
     }
   }
   GvMotion r;
