@@ -41,3 +41,29 @@ def test_streaming_matches_direct():
     # the shifted inputs really produce different results
     assert not torch.equal(results[0], results[1])
     assert torch.equal(results[0], results[3])
+
+
+def test_trkf_batch_to_device(tmp_path):
+    """§8(f) row 3: TRKF files -> one pinned batch (fileio.load_trkf_batch) -> asynchronous H2D
+    (fileio.upload_tracks) -> the fused path gives the same result as the in-memory tracks."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_02586_b200 import fileio
+    from paper_2604_02586_b200.engine import FrameEngine
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    t32 = target.astype(np.float32)
+    paths = []
+    for v in range(len(t32)):
+        paths.append(tmp_path / fileio.track_filename(v, 1))
+        fileio.save_trkf_arrays(paths[-1], v, t32[v], valid[v])
+    th, vh, ids = fileio.load_trkf_batch(paths)
+    assert th.is_pinned() and vh.is_pinned() and ids == list(range(len(t32)))
+    stream = torch.cuda.Stream()
+    td, vd = fileio.upload_tracks(th, vh, stream)
+    torch.cuda.current_stream().wait_stream(stream)
+    eng = FrameEngine().bin(d["gaussians"], d["cameras"])
+    a = eng.compensate(td, vd)
+    b = eng.compensate(t32, valid.astype(np.uint8))
+    for k in ("delta_mean", "rotation", "scale", "status", "weight_sum", "pixel_count"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
