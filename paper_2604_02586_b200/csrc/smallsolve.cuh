@@ -291,6 +291,22 @@ TS_HD int cov_from_r(const double (&R)[6][6], const double (&c6)[6], double *sol
       need_svd = !(1.0 >= 1.0000001 * TS_SINGULAR_GAP_REL * sqrt(fro * finv));
     }
   }
+  if (need_svd) {
+    // Rigorous "certainly rank deficient" test: for triangular R, s_min <= min_i |R_ii| (the
+    // diagonal holds the eigenvalues) and s_max >= every row norm.  Stacked systems that are
+    // truly singular (s_min/s_max ~ 1e-16, all the undecided cases seen in practice) fail here
+    // without an SVD.
+    double dmin = fabs(R[0][0]), rmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+      dmin = fmin(dmin, fabs(R[i][i]));
+      double r2 = 0.0;
+#pragma unroll
+      for (int j = i; j < 6; j++) r2 = fma(R[i][j], R[i][j], r2);
+      rmax = fmax(rmax, sqrt(r2));
+    }
+    if (dmin < TS_SINGULAR_GAP_REL * rmax * (1.0 - 1e-12)) return TS_FUSE_FAIL;
+  }
   if (need_svd && !allow_slow) return TS_FUSE_DEFER;
   if (need_svd) {
     double B[6][6], s[6];
