@@ -189,14 +189,16 @@ class StreamingEngine:
     are in its host buffer (None for the first call); `flush()` runs the last pending step.
     """
 
+    N_SLOTS = 3  # input slots: the copy of step k+1 never waits for step k-1's compute
+
     def __init__(self, engine: FrameEngine | None = None):
         torch = _torch()
         self.eng = engine if engine is not None else FrameEngine()
         self.copy_stream = torch.cuda.Stream()
         self.comp_stream = torch.cuda.Stream()
         self.d2h_stream = torch.cuda.Stream()
-        self._slots = [None, None]
-        self._free = [None, None]      # input slot i reusable after this compute event
+        self._slots = [None] * self.N_SLOTS
+        self._free = [None] * self.N_SLOTS  # input slot i reusable after this compute event
         self._outs = [None, None]
         self._out_free = [None, None]  # output buffer j reusable after this D2H event
         self._k = 0
@@ -253,7 +255,7 @@ class StreamingEngine:
     def step(self, g_host, cameras, t_host, v_host, res_host, config=None):
         """Enqueue the H2D copy of this step's inputs, then compute the previous step."""
         torch = _torch()
-        i = self._k % 2
+        i = self._k % self.N_SLOTS
         self._k += 1
         g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host)
         with torch.cuda.stream(self.copy_stream):
