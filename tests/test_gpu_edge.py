@@ -1,0 +1,123 @@
+"""Edge cases of the fused path (K1-K4) against the CPU oracle and the reference's error rules:
+all-invalid and NaN-at-invalid tracks, identity tracks, a single Gaussian / single view, images
+whose sides are not multiples of the 16-pixel tile, Gaussians behind or outside every camera,
+view-count limits and shape errors."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from tests import golden_data as gd  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def scene7():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    return d["gaussians"], d["cameras"], target, valid
+
+
+def _run(g, cams, target, valid):
+    from paper_2604_02586_b200.engine import FrameEngine
+    eng = FrameEngine().bin(g, cams)
+    out = eng.compensate(target, valid.astype(np.uint8))
+    torch.cuda.synchronize()
+    return out
+
+
+def test_all_invalid_tracks(scene7):
+    g, cams, target, valid = scene7
+    out = _run(g, cams, target.astype(np.float32), np.zeros_like(valid))
+    assert int(out.pixel_count.sum()) == 0 and int(out.static_pixel_count.sum()) == 0
+    assert bool((out.motion_status == 0).all()) and bool((out.status == 0).all())
+    np.testing.assert_array_equal(out.rotation.cpu().numpy(), g[:, 3:7])
+    np.testing.assert_array_equal(out.scale.cpu().numpy(), g[:, 7:10])
+    assert float(out.weight_sum.abs().sum()) == 0.0
+
+
+def test_nan_targets_at_invalid_pixels_are_ignored(scene7):
+    """TrackField allows non-finite targets where invalid (motion2d.py:50-51)."""
+    g, cams, target, valid = scene7
+    t_nan = target.copy()
+    t_nan[~valid] = np.nan
+    a = _run(g, cams, target, valid)
+    b = _run(g, cams, t_nan, valid)
+    for k in ("status", "delta_mean", "rotation", "scale", "pixel_count", "weight_sum"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_identity_tracks_recover_no_motion(scene7):
+    g, cams, target, valid = scene7
+    v, h, w = valid.shape
+    ys, xs = np.mgrid[0:h, 0:w]
+    ident = np.broadcast_to(np.stack([xs, ys], -1).astype(np.float32), (v, h, w, 2)).copy()
+    out = _run(g, cams, ident, valid)
+    st = out.status.cpu().numpy()
+    assert (st == 1).sum() > 0.5 * len(g)
+    d = out.delta_mean.cpu().numpy()[st == 1]
+    assert np.abs(d).max() < 1e-6
+    # every tracked pixel is static (|x' - x| = 0 < 1 px)
+    np.testing.assert_array_equal(out.static_pixel_count.cpu().numpy(),
+                                  out.pixel_count.cpu().numpy())
+
+
+def test_single_gaussian_and_single_view(scene7):
+    g, cams, target, valid = scene7
+    out = _run(g[:1], cams[:1], target[:1], valid[:1])
+    assert out.status.shape == (1,) and int(out.status[0]) == 0  # min_views = 2
+    acc = oracle.accumulate(oracle.rasterize(g[:1], cams[0]), target[0], valid[0], 1)
+    assert int(out.pixel_count[0]) == int(acc["pixel_count"][0])
+
+
+def test_odd_image_size_vs_oracle():
+    """37x29 images: partial tiles on the right and bottom edges."""
+    from paper_2604_02586_b200.scene import generate_scene, oracle_tracks
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    sc = generate_scene(5, 300, 4, 2, focal=30, width=37, height=29, scale_range=(0.02, 0.05))
+    tgt, val = oracle_tracks(sc, 1)
+    cams = np.array([c.as_row() for c in sc.cameras])
+    t_np, v_np = tgt.cpu().numpy().astype(np.float64), val.cpu().numpy().astype(bool)
+    out = _run(sc.frames[0], cams, tgt.cpu().numpy(), v_np)
+    upd, mots, accs = oracle.compensate(sc.frames[0], cams, list(t_np), list(v_np))
+    n = len(sc.frames[0])
+    np.testing.assert_array_equal(out.pixel_count.cpu().numpy().reshape(4, n),
+                                  np.stack([a["pixel_count"] for a in accs]))
+    assert int(out.pixel_count.sum()) > 0
+    np.testing.assert_array_equal(out.status.cpu().numpy(), upd["status"])
+
+
+def test_gaussians_behind_and_outside_cameras(scene7):
+    """Gaussians behind every camera or far outside the frustum are never binned and end
+    UNSOLVABLE with frame-1 parameters; the rest of the frame is unaffected."""
+    g, cams, target, valid = scene7
+    extra = g[:3].copy()
+    extra[0, 0:3] = [0.0, 0.0, 500.0]    # far above the ring: off every image
+    extra[1, 0:3] = [1e4, 1e4, 0.0]      # far away behind / off
+    extra[2, 7:10] = 1e-9                # sub-pixel, below the alpha cutoff everywhere
+    g2 = np.concatenate([g, extra])
+    out = _run(g2, cams, target, valid)
+    st = out.status.cpu().numpy()
+    assert (st[-3:] == 0).all()
+    base = _run(g, cams, target, valid)
+    np.testing.assert_array_equal(st[:-3], base.status.cpu().numpy())
+
+
+def test_argument_errors(scene7):
+    from paper_2604_02586_b200.engine import FrameEngine
+    from paper_2604_02586_b200.errors import DimensionMismatch
+    g, cams, target, valid = scene7
+    eng = FrameEngine().bin(g, cams)
+    with pytest.raises(DimensionMismatch):
+        eng.compensate(target[:, :-1], valid[:, :-1].astype(np.uint8))
+    with pytest.raises(DimensionMismatch):
+        eng.compensate(target[:2], valid[:2].astype(np.uint8))
+    many = np.repeat(cams[:1], 65, axis=0)
+    with pytest.raises(ValueError):
+        FrameEngine().bin(g[:10], many)
