@@ -98,6 +98,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_live(self, timeout=2.0):
+        """Block until nvidia-smi has produced a first sample (its start-up takes ~0.1-0.5 s),
+        then drop it so the summary covers the timed region only."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.lines.clear()
+
     def __exit__(self, *exc):
         if self.proc:
             self.proc.terminate()
@@ -268,6 +276,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.wait_live()
         ev0.record(stream)
         for _ in range(args.steps):
             out = step(out)
@@ -377,17 +386,30 @@ def run_reference(args):
     scene, tracks = make_inputs(args.config, c["gap"] + 1)
     frame = c["gap"]
     procs = len(os.sched_getaffinity(0))
-    vals = []
+    # Each step is a bounded CPU sample of several seconds; the repetitions are capped so the
+    # whole arm stays within ~3 minutes whatever --steps/--warmup ask for (the line reports the
+    # steps actually run).
+    budget_s, t_start = 180.0, time.time()
+    vals, done_warm = [], 0
     for i in range(args.warmup + args.steps):
+        t0 = time.time()
         cb = cpu_baseline(scene, tracks, frame, args.cpu_views, args.cpu_fuse, procs)
-        if i >= args.warmup:
+        if i < args.warmup and done_warm < 1:
+            done_warm += 1
+        else:
             vals.append(cb)
+        per = time.time() - t0
+        if len(vals) >= 1 and time.time() - t_start + per > budget_s:
+            break
+        if i + 1 >= done_warm + args.steps:
+            break
     value = float(np.mean([v["value"] for v in vals]))
     ms = n * nv / value * 1e3
     w, h = scene.cameras[0].width, scene.cameras[0].height
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gaussian-views/s",
-            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(vals),
+            "warmup": done_warm, "steps_requested": args.steps, "ms_per_step": ms,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
             "config": {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w,
@@ -402,8 +424,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)  # ~0.5 s timed: several clock samples
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-views", type=int, default=8)
