@@ -101,8 +101,8 @@ int ts_plan_timing_read(ts_plan *plan, double *totals_ms, int32_t *counts, int32
 int ts_project(const double *gaussians, int64_t n, const ts_camera *camera, double *mean2,
                double *depth, double *cov2, uint8_t *in_front, void *stream);
 
-/* ---- frame engine: the fused hot path (compensate_frame, pipeline.py:110-129 minus
- *      regularisation).  Binning is per clip (it depends only on frame-1 Gaussians and cameras,
+/* ---- frame engine: the fused hot path (the four stages of compensate_frame, pipeline.py:117-124
+ *      and :79-86; the regularisation tail is ts_regularize below).  Binning is per clip (it depends only on frame-1 Gaussians and cameras,
  *      as the weight maps in pipeline.py:191-196); accumulate/solve/fuse runs per target frame. */
 
 /* K1 projection + depth order + tile binning of N Gaussians into V views (all views must share

@@ -16,8 +16,9 @@
 //   * Predicates in fp64 in the reference's operation order (bit-exact q and alpha >= cutoff;
 //     T >= early_stop up to the reference's own log-cumsum rounding).
 //   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp [8 x 64]
-//     shared buffer; every 8 evaluated Gaussians, lane l sums Gaussian (l & 7)'s contributions
-//     over pixel quarter (l >> 3) in pixel order, two xor-shuffle steps add the quarters (exactly
+//     shared buffer; every 8 contributing Gaussians (across chunk boundaries; k2_flush), lane l
+//     sums Gaussian (l & 7)'s contributions over pixel quarter (l >> 3) in pixel order, two
+//     xor-shuffle steps add the quarters (exactly
 //     commutative pairs, so every lane holds the same bits), and the anchored moments go to the
 //     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
 //     bit-reproducible (K3 adds the sub-slots in fixed order).
