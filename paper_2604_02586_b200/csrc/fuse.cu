@@ -58,15 +58,18 @@ __device__ __forceinline__ void store_updates(ts_updates u, int64_t g, const dou
 __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int64_t n, int V,
                                                ts_motions m, ts_config cfg, ts_updates u,
                                                uint32_t *__restrict__ key,
-                                               uint32_t *__restrict__ val) {
+                                               uint32_t *__restrict__ val,
+                                               uint64_t *__restrict__ solved_mask) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
   int n_solved = 0;
   double tw = 0.0;
   int64_t tp = 0;
+  uint64_t mask = 0;
   for (int v = 0; v < V; v++) {
     const int64_t gv = (int64_t)v * n + g;
     if (m.status[gv] != TS_STATUS_SOLVED) continue;
+    mask |= 1ull << v;
     n_solved++;
     tw += m.weight_sum[gv];
     tp += m.pixel_count[gv];
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
                   tp >= cfg.min_total_pixels;
   key[g] = ok ? (uint32_t)n_solved : 0xFFu;
   val[g] = (uint32_t)g;
+  solved_mask[g] = ok ? mask : 0ull;
   if (!ok) {
     double delta[3] = {0.0, 0.0, 0.0}, q[4], sc[3];
 #pragma unroll
@@ -90,6 +94,7 @@ __global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *_
                                                ts_motions m, ts_config cfg, ts_updates u,
                                                const uint32_t *__restrict__ order_key,
                                                const uint32_t *__restrict__ order,
+                                               const uint64_t *__restrict__ solved_mask,
                                                K4Deferred *defer, unsigned *n_defer) {
   extern __shared__ ts_camera s_cam4[];
   for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam4[i] = cams[i];
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *_
 #pragma unroll
   for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
   double delta[3], q[4], sc[3], R4[4][4], R6[6][6], c6[6];
-  const int status = fuse_gaussian(gs, g, n, s_cam4, V, m, cfg, delta, q, sc, R4, R6, c6, false);
+  const int status = fuse_gaussian(gs, g, n, s_cam4, V, m, cfg, delta, q, sc, R4, R6, c6, false,
+                                   nullptr, solved_mask[g]);
   if (status == TS_FUSE_DEFER_STATUS) {
     K4Deferred *d = defer + atomicAdd(n_defer, 1u);
     int k = 0;
@@ -254,7 +260,7 @@ static size_t k4_sort_temp_bytes(int64_t n) {
 }
 size_t k4_workspace_bytes(int64_t n) {
   return 256 + align256(sizeof(K4Deferred) * (size_t)n) + 4 * align256(4 * (size_t)n) +
-         align256(k4_sort_temp_bytes(n));
+         align256(8 * (size_t)n) + align256(k4_sort_temp_bytes(n));
 }
 
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
@@ -266,13 +272,14 @@ void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts
   char *kv = ws + 256 + align256(sizeof(K4Deferred) * (size_t)n);
   uint32_t *key = reinterpret_cast<uint32_t *>(kv), *val = key + align256(4 * (size_t)n) / 4;
   uint32_t *key2 = val + align256(4 * (size_t)n) / 4, *val2 = key2 + align256(4 * (size_t)n) / 4;
-  void *tmp = val2 + align256(4 * (size_t)n) / 4;
+  uint64_t *mask = reinterpret_cast<uint64_t *>(val2 + align256(4 * (size_t)n) / 4);
+  void *tmp = reinterpret_cast<char *>(mask) + align256(8 * (size_t)n);
   size_t tmp_bytes = k4_sort_temp_bytes(n);
   cudaMemsetAsync(n_defer, 0, sizeof(unsigned), s);
-  k4_prep<<<blocks(n, 256), 256, 0, s>>>(G, n, V, m, cfg, u, key, val);
+  k4_prep<<<blocks(n, 256), 256, 0, s>>>(G, n, V, m, cfg, u, key, val, mask);
   cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, val, val2, (int)n, 0, 8, s);
   k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u, key2, val2,
-                                                              defer, n_defer);
+                                                              mask, defer, n_defer);
   const unsigned fin_blocks = (unsigned)std::min<int64_t>(blocks(n, 128), 148 * 4);
   k4_finish<<<fin_blocks, 128, 0, s>>>(G, cfg, u, defer, n_defer);
 }

@@ -563,10 +563,12 @@ TS_HD int fuse_finish(const double *gs, const double (&R4)[4][4], const double (
 // Gaussian g (stride n between views) and writes its update; returns the status.
 // With allow_slow == false the SVD-deciding Gaussians return TS_FUSE_DEFER_STATUS and leave their
 // R factors in R4 / R6 / c6 for fuse_finish in the deferred pass.
+// `eligible_mask` != 0: the caller already applied the eligibility rule and passes the SOLVED-view
+// bits (k4_prep), so the per-view status / weight / count reads are not repeated.
 TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera *cams, int V,
                         const ts_motions &m, const ts_config &cfg, double *delta, double *q,
                         double *sc, double (&R4)[4][4], double (&R6)[6][6], double (&c6)[6],
-                        bool allow_slow, double *dbg = nullptr) {
+                        bool allow_slow, double *dbg = nullptr, uint64_t eligible_mask = 0) {
   double c3[9];
   covariance3d(gs, c3);
 #pragma unroll
@@ -581,18 +583,6 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   }
   // eligibility pre-pass (multiview.py:231-235): cheap loads only, so Gaussians with too few
   // solved views never touch the heavy math
-  int n_solved = 0;
-  double tw = 0.0;
-  int64_t tp = 0;
-  uint64_t solved = 0;  // bit v: view v SOLVED (V <= 64)
-  for (int v = 0; v < V; v++) {
-    const int64_t gv = (int64_t)v * n + g;
-    if (m.status[gv] != TS_STATUS_SOLVED) continue;
-    solved |= 1ull << v;
-    n_solved++;
-    tw += m.weight_sum[gv];
-    tp += m.pixel_count[gv];
-  }
 #pragma unroll
   for (int i = 0; i < 3; i++) {
     delta[i] = 0.0;
@@ -600,8 +590,23 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   }
 #pragma unroll
   for (int i = 0; i < 4; i++) q[i] = gs[3 + i];
-  if (!(n_solved >= cfg.min_views && tw >= cfg.min_total_weight && tp >= cfg.min_total_pixels))
-    return TS_STATUS_UNSOLVABLE;
+  uint64_t solved = eligible_mask;  // bit v: view v SOLVED (V <= 64)
+  if (!solved) {
+    int n_solved = 0;
+    double tw = 0.0;
+    int64_t tp = 0;
+    for (int v = 0; v < V; v++) {
+      const int64_t gv = (int64_t)v * n + g;
+      if (m.status[gv] != TS_STATUS_SOLVED) continue;
+      solved |= 1ull << v;
+      n_solved++;
+      tw += m.weight_sum[gv];
+      tp += m.pixel_count[gv];
+    }
+    if (!(n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
+          tp >= cfg.min_total_pixels))
+      return TS_STATUS_UNSOLVABLE;
+  }
   bool bad = false;
   // iterate the solved views only, in view order: Gaussians with equal solved-view counts (k4_fuse
   // groups them) then run the heavy body in lockstep
