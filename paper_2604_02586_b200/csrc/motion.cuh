@@ -88,47 +88,55 @@ struct GvMotion {
   int8_t status;
 };
 
-// Sum the (instance, quadrant) sub-slots of one gv in fixed order and fit its affine motion.
-TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t base4,
-                        uint32_t nslots, int anchor_x, int anchor_y, double det_floor,
-                        int min_pixels, double min_weight) {
-  double mom[TS_NMOM];
+// Add the flagged sub-slot of instance slot base (4 sub-slots per flag word) to the moments.
+TS_HD void add_slot(const Partial *partial, uint32_t slot, double (&mom)[TS_NMOM], uint32_t &cnt,
+                    uint32_t &scnt) {
+  const double2 *p2 = reinterpret_cast<const double2 *>(partial + slot);
+  double2 v[7];  // m[0..12] and (count, static_count) in the low / high words of v[6].y
 #pragma unroll
-  for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
-  uint32_t cnt = 0, scnt = 0;
-  // nslots is a multiple of TS_K2_SUBS = 4 and base4 is 4-aligned: one 32-bit word holds the
-  // flags of an instance's four quadrant sub-slots; records are read as 16-byte vectors
+  for (int k = 0; k < 7; k++) v[k] = p2[k];
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    mom[2 * k] += v[k].x;
+    mom[2 * k + 1] += v[k].y;
+  }
+  mom[12] += v[6].x;
+  const uint64_t counts = double_bits(v[6].y);
+  cnt += (uint32_t)counts;
+  scnt += (uint32_t)(counts >> 32);
+}
+
+// Add the flagged sub-slots of instances [i_begin, i_end) (step `stride`) of one gv, in order.
+// base4 = 4 * first instance; one 32-bit flag word per instance holds its four quadrant flags;
+// four words per round keep independent loads in flight for large bboxes.
+TS_HD void accumulate_slots(const Partial *partial, const uint8_t *flag, uint32_t base4,
+                            uint32_t i_begin, uint32_t i_end, uint32_t stride,
+                            double (&mom)[TS_NMOM], uint32_t &cnt, uint32_t &scnt) {
   static_assert(TS_K2_SUBS == 4, "flag words assume four sub-slots per instance");
-  for (uint32_t i0 = 0; i0 < nslots; i0 += 16) {
-    // four instances' flag words per round: independent loads in flight for large bboxes
+  for (uint32_t i0 = i_begin; i0 < i_end; i0 += 4 * stride) {
     uint32_t fw[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++)
-      fw[q] = i0 + 4 * q < nslots
-                  ? *reinterpret_cast<const uint32_t *>(flag + base4 + i0 + 4 * q) : 0u;
+    for (int q = 0; q < 4; q++) {
+      const uint32_t inst = i0 + q * stride;
+      fw[q] = inst < i_end ? *reinterpret_cast<const uint32_t *>(flag + base4 + 4 * inst) : 0u;
+    }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-    const uint32_t i = i0 + 4 * q;
-    uint32_t f4 = fw[q];
-    while (f4) {
-      const int sub = (ffs_hd(f4) - 1) >> 3;
-      f4 &= ~(0xFFu << (8 * sub));
-      const double2 *p2 = reinterpret_cast<const double2 *>(partial + base4 + i + sub);
-      double2 v[7];  // m[0..12] and (count, static_count) in the low / high words of v[6].y
-#pragma unroll
-      for (int k = 0; k < 7; k++) v[k] = p2[k];
-#pragma unroll
-      for (int k = 0; k < 6; k++) {
-        mom[2 * k] += v[k].x;
-        mom[2 * k + 1] += v[k].y;
+      const uint32_t slot0 = base4 + 4 * (i0 + q * stride);
+      uint32_t f4 = fw[q];
+      while (f4) {
+        const int sub = (ffs_hd(f4) - 1) >> 3;
+        f4 &= ~(0xFFu << (8 * sub));
+        add_slot(partial, slot0 + sub, mom, cnt, scnt);
       }
-      mom[12] += v[6].x;
-      const uint64_t counts = double_bits(v[6].y);
-      cnt += (uint32_t)counts;
-      scnt += (uint32_t)(counts >> 32);
-    }
     }
   }
+}
+
+// Affine fit of one gv from its summed anchored moments (motion2d.py:164-184).
+TS_HD GvMotion solve_moments(const double (&mom)[TS_NMOM], uint32_t cnt, uint32_t scnt,
+                             int anchor_x, int anchor_y, double det_floor, int min_pixels,
+                             double min_weight) {
   GvMotion r;
   r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
   r.b[0] = 0.0; r.b[1] = 0.0;
@@ -156,6 +164,18 @@ TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t ba
     }
   }
   return r;
+}
+
+// Sum the (instance, quadrant) sub-slots of one gv in fixed order and fit its affine motion.
+TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t base4,
+                        uint32_t nslots, int anchor_x, int anchor_y, double det_floor,
+                        int min_pixels, double min_weight) {
+  double mom[TS_NMOM];
+#pragma unroll
+  for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
+  uint32_t cnt = 0, scnt = 0;
+  accumulate_slots(partial, flag, base4, 0, nslots / 4, 1, mom, cnt, scnt);
+  return solve_moments(mom, cnt, scnt, anchor_x, anchor_y, det_floor, min_pixels, min_weight);
 }
 
 }  // namespace ts

@@ -25,6 +25,20 @@ __device__ __forceinline__ bool finite6(const double *x) {
   return ok;
 }
 
+// A gv with more instances than this is summed by its whole warp (k3_solve).
+constexpr uint32_t K3_BIG = 8;
+
+__device__ __forceinline__ void store_motion(ts_motions m, int64_t gv, const GvMotion &r) {
+  m.status[gv] = r.status;
+  reinterpret_cast<double2 *>(m.a)[2 * gv] = make_double2(r.a[0], r.a[1]);
+  reinterpret_cast<double2 *>(m.a)[2 * gv + 1] = make_double2(r.a[2], r.a[3]);
+  reinterpret_cast<double2 *>(m.b)[gv] = make_double2(r.b[0], r.b[1]);
+  m.weight_sum[gv] = r.wsum;
+  m.pixel_count[gv] = (int32_t)r.count;
+  if (m.static_pixel_count) m.static_pixel_count[gv] = (int32_t)r.static_count;
+  if (m.static_weight_sum) m.static_weight_sum[gv] = r.static_wsum;
+}
+
 #ifndef TS_K3_MIN_BLOCKS
 #define TS_K3_MIN_BLOCKS 4
 #endif
@@ -35,25 +49,49 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial 
                                                 const int16_t *__restrict__ bbox,
                                                 int64_t NV, double det_floor, int min_pixels,
                                                 double min_weight, ts_motions m) {
-  int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gv >= NV) return;
-  const uint32_t nt = ntiles[gv];
-  GvMotion r;
+  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = gv < NV;
+  const uint32_t nt = valid ? ntiles[gv] : 0u;
+  // gvs with many instances (large bboxes) are summed by the whole warp afterwards, so one
+  // straggler no longer holds its 31 neighbours (lane i takes instances i, i+32, ...; the lanes
+  // then combine in a fixed xor tree: deterministic)
+  const bool big = nt > K3_BIG;
+  uint32_t base4 = 0;
+  int ax = 0, ay = 0;
   if (nt) {
     const short4 bb = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
-    r = solve_gv(partial, flag, TS_K2_SUBS * inst_base[gv], TS_K2_SUBS * nt, ((int)bb.x + (int)bb.y) >> 1,
-                 ((int)bb.z + (int)bb.w) >> 1, det_floor, min_pixels, min_weight);
-  } else {
-    r = solve_gv(partial, flag, 0, 0, 0, 0, det_floor, min_pixels, min_weight);
+    base4 = TS_K2_SUBS * inst_base[gv];
+    ax = ((int)bb.x + (int)bb.y) >> 1;
+    ay = ((int)bb.z + (int)bb.w) >> 1;
   }
-  m.status[gv] = r.status;
-  reinterpret_cast<double2 *>(m.a)[2 * gv] = make_double2(r.a[0], r.a[1]);
-  reinterpret_cast<double2 *>(m.a)[2 * gv + 1] = make_double2(r.a[2], r.a[3]);
-  reinterpret_cast<double2 *>(m.b)[gv] = make_double2(r.b[0], r.b[1]);
-  m.weight_sum[gv] = r.wsum;
-  m.pixel_count[gv] = (int32_t)r.count;
-  if (m.static_pixel_count) m.static_pixel_count[gv] = (int32_t)r.static_count;
-  if (m.static_weight_sum) m.static_weight_sum[gv] = r.static_wsum;
+  if (valid && !big) {
+    const GvMotion r = solve_gv(partial, flag, base4, TS_K2_SUBS * nt, ax, ay, det_floor,
+                                min_pixels, min_weight);
+    store_motion(m, gv, r);
+  }
+  uint32_t bigmask = __ballot_sync(0xffffffffu, valid && big);
+  while (bigmask) {
+    const int j = __ffs(bigmask) - 1;
+    bigmask &= bigmask - 1;
+    const uint32_t ntj = __shfl_sync(0xffffffffu, nt, j);
+    const uint32_t b4j = __shfl_sync(0xffffffffu, base4, j);
+    double mom[TS_NMOM];
+#pragma unroll
+    for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
+    uint32_t cnt = 0, scnt = 0;
+    accumulate_slots(partial, flag, b4j, lane, ntj, 32, mom, cnt, scnt);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int k = 0; k < TS_NMOM; k++) mom[k] += __shfl_xor_sync(0xffffffffu, mom[k], d);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+      scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
+    }
+    if (lane == j)
+      store_motion(m, gv, solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels,
+                                        min_weight));
+  }
 }
 
 // solve_view on absolute moments (motion2d.py:164-184).
