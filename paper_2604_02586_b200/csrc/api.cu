@@ -66,7 +66,7 @@ struct ts_plan {
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
   // regularisation buffers
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
-      reg_static, reg_source, reg_euler, k4_ws, drange;
+      reg_static, reg_source, reg_euler, k4_ws, drange, k2_sched;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
   int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
@@ -120,7 +120,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end,
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
-                          &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange};
+                          &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -137,7 +137,7 @@ void release_all(ts_plan *p) {
                     &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
-                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange};
+                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -448,6 +448,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.weight_sum) m.weight_sum = im.weight_sum;
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
+  ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
   cudaEvent_t e3 = p->mark_begin(s);
   TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, TS_K2_SUBS * (ni + 1), s));
   TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
@@ -455,7 +456,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,
                         track_target, track_valid, p->W, p->H, p->tiles_x, p->tpv, p->cfg,
                         ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
-                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, k2_stats(p, s), s));
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, k2_stats(p, s),
+                        p->k2_sched.p, s));
   k2_stats_report(p, s);
   p->mark_end(ST_RASTER, e3, s);
 
@@ -532,7 +534,8 @@ int ts_rasterize_weights(ts_plan *p, const double *gaussians, int64_t n, const t
                           nullptr, p->W, p->H, p->tiles_x, p->tpv, cfg, nullptr, nullptr,
                           ptr<unsigned long long>(p->emit_count), cap, ptr<uint64_t>(p->emit_key),
                           ptr<uint32_t>(p->emit_gv), ptr<double>(p->emit_alpha),
-                          ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, nullptr, s));
+                          ptr<double>(p->emit_trans), nullptr, nullptr, nullptr, nullptr,
+                          nullptr, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, p->emit_count.p, 8, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 2, p->deg_count.p, 8, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
@@ -700,7 +703,7 @@ int ts_dominant_gaussians(ts_plan *p, int32_t view, int64_t *gid_img, double *de
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), view * p->tpv,
                         (view + 1) * p->tpv, nullptr, nullptr, p->W, p->H, p->tiles_x, p->tpv,
                         p->cfg, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
-                        ptr<double>(p->depth64), gid_img, depth_img, nullptr, s));
+                        ptr<double>(p->depth64), gid_img, depth_img, nullptr, nullptr, s));
   return TS_OK;
 }
 

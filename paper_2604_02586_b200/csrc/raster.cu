@@ -22,6 +22,8 @@
 //     commutative pairs, so every lane holds the same bits), and the anchored moments go to the
 //     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
 //     bit-reproducible (K3 adds the sub-slots in fixed order).
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -412,6 +414,39 @@ __global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, 
   if (ne) items[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)t;
 }
 
+// Work-ordered schedule (accumulate mode): every tile keyed by its list length (in units of 32
+// instances, capped at 255); a one-pass descending radix sort puts the longest tiles at the head
+// of the atomic queue, so the long lists start first and the kernel does not end on a tail of
+// a few heavy units (longest-processing-time-first).
+__global__ void k2_tile_keys(const uint32_t *__restrict__ tile_range, int t0, int t1,
+                             uint8_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                             uint32_t *__restrict__ n_items) {
+  const int t = t0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t len = t < t1 ? tile_range[2 * t + 1] - tile_range[2 * t] : 0u;
+  const bool ne = t < t1 && tile_range[2 * t] < tile_range[2 * t + 1];
+  if (t < t1) {
+    keys[t - t0] = (uint8_t)min(len / 32u + (ne ? 1u : 0u), 255u);  // empty tiles: key 0, last
+    vals[t - t0] = (uint32_t)t;
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, ne);
+  if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(n_items, (uint32_t)__popc(m));
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t k2_sort_temp(int nt) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const uint8_t *)nullptr,
+                                            (uint8_t *)nullptr, (const uint32_t *)nullptr,
+                                            (uint32_t *)nullptr, nt, 0, 8);
+  return bytes;
+}
+
+size_t k2_schedule_bytes(int n_tiles) {
+  return 2 * align_up((size_t)n_tiles) + align_up(4 * (size_t)n_tiles) +
+         align_up(k2_sort_temp(n_tiles));
+}
+
 template <int MODE, typename TrackT>
 static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
   auto kern = k2_raster<MODE, TrackT>;
@@ -435,14 +470,27 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      unsigned long long *stats, cudaStream_t s) {
+                      unsigned long long *stats, void *schedule_ws, cudaStream_t s) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int nt = tile_end - tile_begin;
-  if (nt > 0)
+  if (nt > 0 && schedule_ws) {
+    char *ws = reinterpret_cast<char *>(schedule_ws);
+    uint8_t *keys = reinterpret_cast<uint8_t *>(ws);
+    uint8_t *keys2 = reinterpret_cast<uint8_t *>(ws + align_up((size_t)nt));
+    uint32_t *vals = reinterpret_cast<uint32_t *>(ws + 2 * align_up((size_t)nt));
+    void *tmp = ws + 2 * align_up((size_t)nt) + align_up(4 * (size_t)nt);
+    size_t tmp_bytes = k2_sort_temp(nt);
+    k2_tile_keys<<<(nt + 255) / 256, 256, 0, s>>>(tile_range, tile_begin, tile_end, keys, vals,
+                                                  counters);
+    e = cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, keys, keys2, vals, items, nt, 0,
+                                                  8, s);
+    if (e != cudaSuccess) return e;
+  } else if (nt > 0) {
     k2_build_items<<<(nt + 255) / 256, 256, 0, s>>>(tile_range, tile_begin, tile_end, items,
                                                     counters);
+  }
   K2Params P;
   P.rec = rec;
   P.inst_gv = inst_gv;
