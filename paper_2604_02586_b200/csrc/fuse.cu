@@ -52,9 +52,10 @@ __device__ __forceinline__ void store_updates(ts_updates u, int64_t g, const dou
 #define TS_K4_MIN_BLOCKS 3
 #endif
 // Eligibility pre-pass of update_all (multiview.py:231-235): ineligible Gaussians get their
-// UNSOLVABLE update here; eligible ones are keyed by their solved-view count so that a radix sort
-// groups Gaussians of equal work into the same warps of k4_fuse (the streaming QR loops over the
-// solved views: mixed counts and early exits left ~12 of 32 lanes active).
+// UNSOLVABLE update here; eligible ones are keyed by their solved-view count so that a descending
+// radix sort groups Gaussians of equal work into the same warps of k4_fuse, heaviest first (the
+// streaming QR loops over the solved views: mixed counts and early exits left ~12 of 32 lanes
+// active, and the heaviest warps last made a tail).
 __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int64_t n, int V,
                                                ts_motions m, ts_config cfg, ts_updates u,
                                                uint32_t *__restrict__ key,
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
   }
   const bool ok = n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
                   tp >= cfg.min_total_pixels;
-  key[g] = ok ? (uint32_t)n_solved : 0xFFu;
+  key[g] = ok ? (uint32_t)n_solved : 0u;  // descending sort: heaviest first, ineligible last
   val[g] = (uint32_t)g;
   solved_mask[g] = ok ? mask : 0ull;
   if (!ok) {
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *_
   for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam4[i] = cams[i];
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n || order_key[t] == 0xFFu) return;  // ineligible: written by k4_prep
+  if (t >= n || order_key[t] == 0u) return;  // ineligible: written by k4_prep
   const int64_t g = order[t];
   double gs[11];
 #pragma unroll
@@ -254,8 +255,9 @@ void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, t
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static size_t k4_sort_temp_bytes(int64_t n) {
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                  (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n, 0, 8);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const uint32_t *)nullptr,
+                                            (uint32_t *)nullptr, (const uint32_t *)nullptr,
+                                            (uint32_t *)nullptr, (int)n, 0, 8);
   return bytes;
 }
 size_t k4_workspace_bytes(int64_t n) {
@@ -277,7 +279,8 @@ void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts
   size_t tmp_bytes = k4_sort_temp_bytes(n);
   cudaMemsetAsync(n_defer, 0, sizeof(unsigned), s);
   k4_prep<<<blocks(n, 256), 256, 0, s>>>(G, n, V, m, cfg, u, key, val, mask);
-  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, val, val2, (int)n, 0, 8, s);
+  cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, key, key2, val, val2, (int)n, 0, 8,
+                                            s);
   k4_fuse<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, m, cfg, u, key2, val2,
                                                               mask, defer, n_defer);
   const unsigned fin_blocks = (unsigned)std::min<int64_t>(blocks(n, 128), 148 * 4);
