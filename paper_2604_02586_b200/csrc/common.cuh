@@ -224,15 +224,22 @@ TS_HD int lo_int(double d) {
   return (int)(uint32_t)u;
 #endif
 }
+// the polynomial's coefficients as constant-bank operands of DFMA (no per-use UMOV pairs)
+static __constant__ double k_exp_poly[4] = {1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+#ifdef __CUDA_ARCH__
+#define TS_EXP_C(i, v) k_exp_poly[i]
+#else
+#define TS_EXP_C(i, v) (v)
+#endif
 TS_HD double alpha_of_table(double opacity, double q, const double *etab) {
   const double x = mul(-0.5, q);
   // round-to-nearest-even of 64 x with the 1.5*2^52 shifter: stays on the fp64 pipe (no F2F/F2I)
   const double kd = fma(x, 64.0, 6755399441055744.0);
   const double kf = kd - 6755399441055744.0;
   const double r = fma(kf, -0.015625, x);
-  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(r, p, 1.0 / 24.0);
-  p = fma(r, p, 1.0 / 6.0);
+  double p = fma(r, TS_EXP_C(0, 1.0 / 720.0), TS_EXP_C(1, 1.0 / 120.0));
+  p = fma(r, p, TS_EXP_C(2, 1.0 / 24.0));
+  p = fma(r, p, TS_EXP_C(3, 1.0 / 6.0));
   p = fma(r, p, 0.5);
   p = fma(r, p, 1.0);
   p = fma(r, p, 1.0);

@@ -85,6 +85,7 @@ struct K2Warp {
   RasterRec rec[32];
   uint64_t rect[32];  // bbox of the record clipped to the quadrant, as a 64-pixel bit mask
   uint32_t slot[32];
+  int2 anc[32];       // moment anchor (bbox centre pixel) of each record (accumulate mode)
   double w[K2_FLUSH][K2_WROW];
   TrackT trk_u[64], trk_v[64];  // track targets in their input precision
   uint8_t trk_static[64];
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
             const int tx0 = r.x0 / TS_TILE, tx1 = r.x1 / TS_TILE, ty0 = r.y0 / TS_TILE;
             S.slot[lane] = 4u * (P.inst_base[gv] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) +
                                                              (tx - tx0))) + (uint32_t)quad;
+            S.anc[lane] = make_int2(anchor_x(r), anchor_y(r));
           } else {
             S.slot[lane] = gv;
           }
@@ -329,8 +331,9 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
                 const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
                 my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
                 my_slot = S.slot[j];
-                my_ax = anchor_x(r);
-                my_ay = anchor_y(r);
+                const int2 an = S.anc[j];
+                my_ax = an.x;
+                my_ay = an.y;
               }
               if (++kpend == K2_FLUSH) {
                 __syncwarp();
