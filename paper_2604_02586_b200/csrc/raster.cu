@@ -103,9 +103,10 @@ __device__ __forceinline__ uint64_t quad_rect(const RasterRec &r, int qx0, int q
 }
 
 // One pixel of a lane: predicate evaluation and front-to-back compositing (splat.py:147-193).
+// The pixel is saturated ("done") exactly when !(T >= early_stop): T only decreases, so no
+// separate flag is kept (pixels outside the image start at T = 0).
 struct PixelState {
   double T;
-  bool done;
 };
 
 __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double fpx, double fpy,
@@ -121,7 +122,6 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
   const double tin = ps.T;
   w_out = mul(a, tin);  // motion2d.py:151
   ps.T = mul(tin, sub(1.0, a));
-  if (!(ps.T >= early_stop)) ps.done = true;
   a_out = a;
   tin_out = tin;
   return true;
@@ -250,15 +250,15 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         if (h) valid1 = val; else valid0 = val;
       }
     }
-    PixelState s0{1.0, !in0 || !(1.0 >= P.early_stop)};
-    PixelState s1{1.0, !in1 || !(1.0 >= P.early_stop)};
+    PixelState s0{in0 ? 1.0 : 0.0};
+    PixelState s1{in1 ? 1.0 : 0.0};
     uint32_t seq0 = 0, seq1 = 0;                  // emit mode
     double best_w0 = -1.0, best_w1 = -1.0;        // dominant mode
     uint32_t best_g0 = 0xFFFFFFFFu, best_g1 = 0xFFFFFFFFu, best_gv0 = 0, best_gv1 = 0;
 
     // saturated pixels of the quadrant (bit = row * 8 + col), warp-uniform
-    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
-                      ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
+    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, !(s0.T >= P.early_stop)) |
+                      ((uint64_t)__ballot_sync(0xffffffffu, !(s1.T >= P.early_stop)) << 32);
     if (K2_STATS_ON) st[K2S_UNITS]++;
     // pending Gaussians of the transposed reduction (accumulate mode): the lanes with
     // (lane & 7) == k keep Gaussian k's contribution bits of their pixel quarter, its sub-slot
@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
                                      P.early_stop, etab, s0, a0, w0, t0);
           const bool c1 = eval_pixel(r, (cand >> (lane + 32)) & 1ull, fpx, fpy1, P.alpha_cutoff,
                                      P.early_stop, etab, s1, a1, w1, t1);
-          done64 = (uint64_t)__ballot_sync(0xffffffffu, s0.done) |
-                   ((uint64_t)__ballot_sync(0xffffffffu, s1.done) << 32);
+          done64 = (uint64_t)__ballot_sync(0xffffffffu, !(s0.T >= P.early_stop)) |
+                   ((uint64_t)__ballot_sync(0xffffffffu, !(s1.T >= P.early_stop)) << 32);
           if (MODE == K2_ACCUMULATE) {
             const bool k0 = c0 && valid0, k1 = c1 && valid1;
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
