@@ -17,8 +17,8 @@
 //     T >= early_stop up to the reference's own log-cumsum rounding).
 //   * Transposed accumulation: contributing lanes store w = alpha*T into a per-warp [8 x 64]
 //     shared buffer; every 8 contributing Gaussians (across chunk boundaries; k2_flush), lane l
-//     sums Gaussian (l & 7)'s contributions over pixel quarter (l >> 3) in pixel order, two
-//     xor-shuffle steps add the quarters (exactly
+//     sums every fourth contribution of Gaussian (l & 7) in pixel order, two xor-shuffle steps
+//     add the four partial sums (exactly
 //     commutative pairs, so every lane holds the same bits), and the anchored moments go to the
 //     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
 //     bit-reproducible (K3 adds the sub-slots in fixed order).
@@ -127,13 +127,14 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
   return true;
 }
 
-// Transposed reduction of the pending Gaussians (kcount <= K2_FLUSH): lane l sums Gaussian
-// (l & 7)'s contributions over pixel quarter (l >> 3) in pixel order; two xor-shuffle steps add
-// the quarters ((q0 + q1) + (q2 + q3): commutative pairs, so all four lanes hold the same bits)
-// and the anchored moments go to the Gaussian's (instance, quadrant) sub-slot.  Warp-uniform call.
+// Transposed reduction of the pending Gaussians (kcount <= K2_FLUSH): lane l sums every fourth
+// contributing pixel of Gaussian (l & 7), starting at its (l >> 3)-th, in pixel order; two
+// xor-shuffle steps add the four partial sums ((s0 + s1) + (s2 + s3): commutative pairs, so all
+// four lanes hold the same bits) and the anchored moments go to the Gaussian's (instance,
+// quadrant) sub-slot.  Warp-uniform call.
 template <typename TrackT>
 __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params &P, int lane,
-                                         int kcount, uint32_t my_cm, uint32_t my_slot, int my_ax,
+                                         int kcount, uint64_t my_cm, uint32_t my_slot, int my_ax,
                                          int my_ay, int qx0, int qy0) {
   const int kk = lane & 7, qq = lane >> 3;
   double m[TS_NMOM];
@@ -143,9 +144,15 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
   if (my_cm) {
     const double ax = (double)my_ax, ay = (double)my_ay;
     const double bx = (double)(qx0 - my_ax), by = (double)(qy0 - my_ay);
-    uint32_t bits = my_cm;
+    // the four lanes of Gaussian kk take every fourth of its contributing pixels (lane qq
+    // starts at the qq-th): balanced trip counts whatever the pixels' rows
+    uint64_t bits = my_cm;
+    for (int k = 0; k < qq; k++) bits &= bits - 1;
     while (bits) {
-      const int p = __ffs(bits) - 1 + 16 * qq;
+      const int p = __ffsll((long long)bits) - 1;
+      bits &= bits - 1;
+      bits &= bits - 1;
+      bits &= bits - 1;
       bits &= bits - 1;
       const double w = S.w[kk][p];
       const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
@@ -264,7 +271,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
     // (lane & 7) == k keep Gaussian k's contribution bits of their pixel quarter, its sub-slot
     // and its anchor; a flush runs every K2_FLUSH evaluated Gaussians, across chunk boundaries
     int kpend = 0;
-    uint32_t my_cm = 0, my_slot = 0;
+    uint64_t my_cm = 0;
+    uint32_t my_slot = 0;
     int my_ax = 0, my_ay = 0;
     for (uint32_t b = start; b < end; b += 32) {
       if (done64 == ~0ull) break;
@@ -327,9 +335,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
             if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
               if (k0) S.w[kpend][lane] = w0;
               if (k1) S.w[kpend][lane + 32] = w1;
-              if ((lane & 7) == kpend) {
-                const int qq = lane >> 3;  // pixel quarter: 0..15, 16..31, 32..47, 48..63
-                my_cm = ((qq < 2 ? cm0 : cm1) >> (16 * (qq & 1))) & 0xFFFFu;
+              if ((lane & 7) == kpend) {  // the four lanes of this Gaussian's flush slot
+                my_cm = (uint64_t)cm0 | ((uint64_t)cm1 << 32);
                 my_slot = S.slot[j];
                 const int2 an = S.anc[j];
                 my_ax = an.x;
