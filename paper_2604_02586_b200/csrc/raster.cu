@@ -136,7 +136,9 @@ template <typename TrackT>
 __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params &P, int lane,
                                          int kcount, uint64_t my_cm, uint32_t my_slot, int my_ax,
                                          int my_ay, int qx0, int qy0) {
-  const int kk = lane & 7, qq = lane >> 3;
+  static_assert(K2_FLUSH == 4 || K2_FLUSH == 8, "flush: 4 or 8 Gaussians x 8 or 4 lanes");
+  constexpr int LPG = 32 / K2_FLUSH;  // lanes per pending Gaussian
+  const int kk = lane & (K2_FLUSH - 1), qq = lane / K2_FLUSH;
   double m[TS_NMOM];
 #pragma unroll
   for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
@@ -144,16 +146,14 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
   if (my_cm) {
     const double ax = (double)my_ax, ay = (double)my_ay;
     const double bx = (double)(qx0 - my_ax), by = (double)(qy0 - my_ay);
-    // the four lanes of Gaussian kk take every fourth of its contributing pixels (lane qq
-    // starts at the qq-th): balanced trip counts whatever the pixels' rows
+    // the LPG lanes of Gaussian kk take every LPG-th of its contributing pixels (lane qq starts
+    // at the qq-th): balanced trip counts whatever the pixels' rows
     uint64_t bits = my_cm;
     for (int k = 0; k < qq; k++) bits &= bits - 1;
     while (bits) {
       const int p = __ffsll((long long)bits) - 1;
-      bits &= bits - 1;
-      bits &= bits - 1;
-      bits &= bits - 1;
-      bits &= bits - 1;
+#pragma unroll
+      for (int k = 0; k < LPG; k++) bits &= bits - 1;
       const double w = S.w[kk][p];
       const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
       const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
@@ -178,15 +178,13 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
     }
   }
 #pragma unroll
-  for (int q = 0; q < TS_NMOM; q++) {
-    m[q] += __shfl_xor_sync(0xffffffffu, m[q], 8);
-    m[q] += __shfl_xor_sync(0xffffffffu, m[q], 16);
+  for (int d = K2_FLUSH; d < 32; d <<= 1) {
+#pragma unroll
+    for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], d);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
   }
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
-  scnt += __shfl_xor_sync(0xffffffffu, scnt, 8);
-  scnt += __shfl_xor_sync(0xffffffffu, scnt, 16);
-  if (kk < kcount && cnt > 0) {
+  if (kk < kcount && cnt > 0 && qq < 4) {
     // the four lanes of a Gaussian hold identical sums: each stores a quarter of the record
     Partial *dst = P.partial + my_slot;
     if (qq == 0) {
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
             if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
               if (k0) S.w[kpend][lane] = w0;
               if (k1) S.w[kpend][lane + 32] = w1;
-              if ((lane & 7) == kpend) {  // the four lanes of this Gaussian's flush slot
+              if ((lane & (K2_FLUSH - 1)) == kpend) {  // this Gaussian's flush lanes
                 my_cm = (uint64_t)cm0 | ((uint64_t)cm1 << 32);
                 my_slot = S.slot[j];
                 const int2 an = S.anc[j];
