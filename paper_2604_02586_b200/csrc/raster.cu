@@ -88,7 +88,6 @@ struct K2Warp {
   int2 anc[32];       // moment anchor (bbox centre pixel) of each record (accumulate mode)
   double w[K2_FLUSH][K2_WROW];
   TrackT trk_u[64], trk_v[64];  // track targets in their input precision
-  uint8_t trk_static[64];
 };
 
 // 64-bit mask (bit = row * 8 + col) of the quadrant pixels inside the record's bbox.
@@ -135,7 +134,7 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
 template <typename TrackT>
 __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params &P, int lane,
                                          int kcount, uint64_t my_cm, uint32_t my_slot, int my_ax,
-                                         int my_ay, int qx0, int qy0) {
+                                         int my_ay, uint64_t static64, int qx0, int qy0) {
   static_assert(K2_FLUSH == 4 || K2_FLUSH == 8, "flush: 4 or 8 Gaussians x 8 or 4 lanes");
   constexpr int LPG = 32 / K2_FLUSH;  // lanes per pending Gaussian
   const int kk = lane & (K2_FLUSH - 1), qq = lane / K2_FLUSH;
@@ -170,10 +169,9 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
       m[9] += wx * va;
       m[10] += wy * ua;
       m[11] += wy * va;
-      if (S.trk_static[p]) {
-        m[12] += w;
-        scnt++;
-      }
+      const bool st = (static64 >> p) & 1ull;
+      m[12] += st ? w : 0.0;
+      scnt += st;
       cnt++;
     }
   }
@@ -233,6 +231,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
     const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
 
     bool valid0 = false, valid1 = false;
+    uint64_t static64 = 0;  // static-pixel bits of the unit (warp-uniform; accumulate mode)
     if (MODE == K2_ACCUMULATE) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
@@ -251,7 +250,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         const int p = lane + 32 * h;
         S.trk_u[p] = u;
         S.trk_v[p] = vv;
-        S.trk_static[p] = val && is_static((double)u, (double)vv, px, py, P.static_thr);
+        const bool st = val && is_static((double)u, (double)vv, px, py, P.static_thr);
+        static64 |= (uint64_t)__ballot_sync(0xffffffffu, st) << (32 * h);
         if (h) valid1 = val; else valid0 = val;
       }
     }
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
               if (++kpend == K2_FLUSH) {
                 __syncwarp();
                 if (K2_STATS_ON) st[K2S_FLUSHES]++;
-                k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0);
+                k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
                 __syncwarp();
                 kpend = 0;
                 my_cm = 0;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
     if (MODE == K2_ACCUMULATE && kpend > 0) {
       __syncwarp();
       if (K2_STATS_ON) st[K2S_FLUSHES]++;
-      k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0);
+      k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
       __syncwarp();
     }
     if (MODE == K2_DOMINANT) {
