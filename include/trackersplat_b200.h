@@ -112,6 +112,11 @@ int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_cam
 
 /* K2 fused raster-accumulate -> K3 per-view affine solve -> K4 multi-view fuse for one target
  * frame.  track_target: (V, H, W, 2) of TS_TRACK_F32/F64; track_valid: (V, H, W) uint8.
+ * The track arrays are both device memory, or both page-locked (pinned) host memory: K2 then
+ * reads only the 8x8 quadrants of occupied tiles in place over PCIe (zero-copy, prefetched one
+ * work unit ahead), about a tenth of the track bytes at the benchmark configs; the host must
+ * not modify them until the frame's work on `stream` completes.  Pageable host memory, or one
+ * array on each side: TS_E_INVALID_ARGUMENT.
  * motions may have NULL members (then only the internal copy is kept); updates must be valid. */
 int ts_frame_compensate(ts_plan *plan, const void *track_target, int32_t track_dtype,
                         const uint8_t *track_valid, const ts_motions *motions,
@@ -132,6 +137,9 @@ typedef struct ts_binning {
   const int16_t *gv_bbox;    /* (V*N, 4) x0 x1 y0 y1                                 */
 } ts_binning;
 int ts_frame_binning(const ts_plan *plan, ts_binning *out);
+/* Number of (view, tile) lists of the last ts_frame_bin that are non-empty (synchronous): K2
+ * reads the 4 x 64 track pixels of each. */
+int ts_frame_occupied_tiles(const ts_plan *plan, int64_t *out);
 
 /* ---- stage entry points (reference-typed API) ---- */
 

@@ -98,6 +98,7 @@ _SIGS = {
     "ts_frame_compensate": ([_vp, _vp, ctypes.c_int32, _vp, ctypes.POINTER(Motions),
                              ctypes.POINTER(Updates), _vp], ctypes.c_int),
     "ts_frame_binning": ([_vp, ctypes.POINTER(Binning)], ctypes.c_int),
+    "ts_frame_occupied_tiles": ([_vp, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "ts_rasterize_weights": ([_vp, _vp, ctypes.c_int64, ctypes.POINTER(Camera), ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_int64),
                               ctypes.POINTER(ctypes.c_int64), _vp], ctypes.c_int),

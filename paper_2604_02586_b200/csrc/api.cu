@@ -197,6 +197,29 @@ int validate_cams(const ts_camera *cams, int V) {
   return TS_OK;
 }
 
+// Address under which kernels read `ptr`: device / managed memory as is (*host = 0); page-locked
+// host memory through its mapped device address (*host = 1).  Pageable host memory cannot be
+// read by a kernel: TS_E_INVALID_ARGUMENT.
+int device_view(const void *ptr, const void **dev, int *host) {
+  if (!ptr) return TS_E_INVALID_ARGUMENT;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return TS_E_INVALID_ARGUMENT;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    *dev = ptr;
+    *host = 0;
+    return TS_OK;
+  }
+  if (a.type == cudaMemoryTypeHost && a.devicePointer) {
+    *dev = a.devicePointer;
+    *host = 1;
+    return TS_OK;
+  }
+  return TS_E_INVALID_ARGUMENT;
+}
+
 // K1 + sorts + ranges into the plan.
 int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int V,
               const ts_config *cfg, cudaStream_t s) {
@@ -428,6 +451,16 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!p || !updates || p->V < 1) return TS_E_INVALID_ARGUMENT;
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
   const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
+  // tracks: device memory, or pinned host memory that K2 reads in place (zero-copy: only the
+  // 8x8 quadrants of occupied tiles cross PCIe, prefetched one work unit ahead)
+  {
+    int kt = 0, kv = 0;
+    int rc = device_view(track_target, &track_target, &kt);
+    if (rc) return rc;
+    rc = device_view(track_valid, reinterpret_cast<const void **>(&track_valid), &kv);
+    if (rc) return rc;
+    if (kt != kv) return TS_E_INVALID_ARGUMENT;  // both on the device or both pinned host
+  }
   ENSURE(p->partial, sizeof(Partial) * TS_K2_SUBS * (ni + 1));
   ENSURE(p->flag, TS_K2_SUBS * (ni + 1));
   ts_motions m = motions ? *motions : ts_motions{};
@@ -475,6 +508,18 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                  p->k4_ws.p, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_FUSE, e5, s);
+  return TS_OK;
+}
+
+int ts_frame_occupied_tiles(const ts_plan *p, int64_t *out) {
+  if (!p || !out) return TS_E_INVALID_ARGUMENT;
+  const int64_t nt = (int64_t)p->tpv * p->V;
+  std::vector<uint32_t> r(2 * nt);
+  if (nt && cudaMemcpy(r.data(), p->range.p, 8 * nt, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return TS_E_CUDA;
+  int64_t c = 0;
+  for (int64_t t = 0; t < nt; t++) c += r[2 * t] < r[2 * t + 1];
+  *out = c;
   return TS_OK;
 }
 

@@ -239,12 +239,17 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         TrackT u = TrackT(0), vv = TrackT(0);
         bool val = false;
         if (h ? in1 : in0) {
+          // valid byte and target issued together (one round trip: the tracks may be pinned
+          // host memory read in place over PCIe, see ts_frame_compensate); plain loads, no
+          // read-only-cache path, so host-mapped pages work
           const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
-          val = P.track_valid[pix] != 0;
-          if (val) {
-            const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
-            u = __ldg(tg);
-            vv = __ldg(tg + 1);
+          const uint8_t vb = P.track_valid[pix];
+          const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
+          const TrackT tu = tg[0], tv = tg[1];
+          val = vb != 0;
+          if (val) {  // invalid targets may be NaN: never used
+            u = tu;
+            vv = tv;
           }
         }
         const int p = lane + 32 * h;

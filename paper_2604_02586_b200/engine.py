@@ -32,6 +32,15 @@ def _torch():
     return torch
 
 
+def _pinned_pair(tgt, val):
+    """True for contiguous page-locked CPU tensors, which kernels may read in place."""
+    torch = _torch()
+    return (isinstance(tgt, torch.Tensor) and isinstance(val, torch.Tensor)
+            and tgt.device.type == "cpu" and val.device.type == "cpu"
+            and tgt.is_contiguous() and val.is_contiguous()
+            and tgt.is_pinned() and val.is_pinned())
+
+
 def as_device(x, dtype, device=None):
     """Host array / tensor -> contiguous CUDA tensor of `dtype` (no copy if already there)."""
     torch = _torch()
@@ -117,6 +126,13 @@ class FrameEngine:
                     status=grab(b.gv_status, nv, np.int8),
                     bbox=grab(b.gv_bbox, nv, np.int16, 4))
 
+    def occupied_tiles(self):
+        """Non-empty (view, tile) lists of the current binning (K2 reads 256 track pixels each)."""
+        c = ctypes.c_int64(0)
+        nat.check(self._lib.ts_frame_occupied_tiles(self.plan.handle, ctypes.byref(c)),
+                  "occupied_tiles")
+        return int(c.value)
+
     # -- K2 + K3 + K4 ----------------------------------------------------------------------
     def alloc_outputs(self):
         torch = _torch()
@@ -139,13 +155,20 @@ class FrameEngine:
         torch = _torch()
         if self._gauss is None:
             raise RuntimeError("FrameEngine.bin() must run before compensate()")
-        tgt = track_target
-        if not isinstance(tgt, torch.Tensor):
+        tgt, val = track_target, track_valid
+        if _pinned_pair(tgt, val):
+            # zero-copy: K2 reads the occupied tiles' quadrants in place (C ABI)
+            if tgt.dtype not in (torch.float32, torch.float64) or val.dtype != torch.uint8:
+                raise TypeError("pinned tracks must be float32/float64 targets and uint8 valid")
+        elif not isinstance(tgt, torch.Tensor):
             tgt = np.asarray(tgt)
             tgt = as_device(tgt, torch.float32 if tgt.dtype == np.float32 else torch.float64)
+            val = as_device(val, torch.uint8)
         else:
             tgt = tgt.contiguous()
-        val = as_device(track_valid, torch.uint8)
+            if tgt.device.type != "cuda":
+                tgt = as_device(tgt, tgt.dtype)
+            val = as_device(val, torch.uint8)
         expect = (self.n_views, self.height, self.width)
         if tuple(tgt.shape) != expect + (2,) or tuple(val.shape) != expect:
             from .errors import DimensionMismatch
@@ -180,20 +203,26 @@ class StreamingEngine:
     """Double-buffered end-to-end driver: pinned host inputs in, pinned host results out.
 
     Three streams: H2D copies, compute, D2H copies.  `step(inputs_k)` enqueues the H2D copy of
-    inputs k and then the compute of the PREVIOUS step (k-1), so the copy of step k is already
-    queued when step k-1's binning briefly synchronises the host (the instance count); the D2H of
-    a step's results runs on its own stream from one of two output buffers, so the compute stream
-    moves on to the next frame at once.  The PCIe transfers of the next frame therefore overlap
-    the whole compute of the current one.  Input slots and output buffers are reused in turn,
+    step k's Gaussians and then the compute of the PREVIOUS step (k-1), so the copy of step k is
+    already queued when step k-1's binning briefly synchronises the host (the instance count);
+    the D2H of a step's results runs on its own stream from one of two output buffers, so the
+    compute stream moves on to the next frame at once.  Tracks given as pinned host tensors are
+    not copied at all (`zero_copy_tracks=True`, the default): K2 reads the 8x8 quadrants of the
+    occupied tiles in place over PCIe, one work unit ahead (about a tenth of the track bytes at
+    the benchmark configs); with `zero_copy_tracks=False` the whole arrays are copied on the H2D
+    stream.  Input slots and output buffers are reused in turn,
     ordered with CUDA events.  `step` returns the event after which the previous step's results
-    are in its host buffer (None for the first call); `flush()` runs the last pending step.
+    are in its host buffer (None for the first call); `flush()` runs the last pending step.  The
+    caller must leave step k's host inputs unchanged until the event returned by the call that
+    computes step k has completed.
     """
 
     N_SLOTS = 3  # input slots: the copy of step k+1 never waits for step k-1's compute
 
-    def __init__(self, engine: FrameEngine | None = None):
+    def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks: bool = True):
         torch = _torch()
         self.eng = engine if engine is not None else FrameEngine()
+        self.zero_copy_tracks = zero_copy_tracks
         self.copy_stream = torch.cuda.Stream()
         self.comp_stream = torch.cuda.Stream()
         self.d2h_stream = torch.cuda.Stream()
@@ -205,15 +234,16 @@ class StreamingEngine:
         self._j = 0
         self._pending = None
 
-    def _slot(self, i, g_host, t_host, v_host):
+    def _slot(self, i, g_host, t_host, v_host, tracks):
         torch = _torch()
         s = self._slots[i]
-        shapes = (tuple(g_host.shape), tuple(t_host.shape), tuple(v_host.shape), t_host.dtype)
+        shapes = (tuple(g_host.shape), tuple(t_host.shape), tuple(v_host.shape), t_host.dtype,
+                  tracks)
         if s is None or s[0] != shapes:
             dev = torch.device("cuda", torch.cuda.current_device())
             s = (shapes, torch.empty(g_host.shape, dtype=torch.float64, device=dev),
-                 torch.empty(t_host.shape, dtype=t_host.dtype, device=dev),
-                 torch.empty(v_host.shape, dtype=torch.uint8, device=dev))
+                 torch.empty(t_host.shape, dtype=t_host.dtype, device=dev) if tracks else None,
+                 torch.empty(v_host.shape, dtype=torch.uint8, device=dev) if tracks else None)
             self._slots[i] = s
         return s[1], s[2], s[3]
 
@@ -225,7 +255,7 @@ class StreamingEngine:
 
     def _compute(self, pending):
         torch = _torch()
-        i, g_d, t_d, v_d, ready, cameras, res_host, config = pending
+        i, g_d, t_d, v_d, staged, ready, cameras, res_host, config = pending
         j = self._j
         self._j ^= 1
         cs = self.comp_stream
@@ -257,16 +287,21 @@ class StreamingEngine:
         torch = _torch()
         i = self._k % self.N_SLOTS
         self._k += 1
-        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host)
+        staged = self.zero_copy_tracks and _pinned_pair(t_host, v_host)
+        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host, not staged)
         with torch.cuda.stream(self.copy_stream):
             if self._free[i] is not None:
                 self.copy_stream.wait_event(self._free[i])
             g_d.copy_(g_host, non_blocking=True)
-            t_d.copy_(t_host, non_blocking=True)
-            v_d.copy_(v_host, non_blocking=True)
+            if staged:
+                t_d, v_d = t_host, v_host  # read in place by K2
+            else:
+                t_d.copy_(t_host, non_blocking=True)
+                v_d.copy_(v_host, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self.copy_stream)
-        prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config)
+        prev, self._pending = self._pending, (i, g_d, t_d, v_d, staged, ready, cameras, res_host,
+                                              config)
         return self._compute(prev) if prev is not None else None
 
     def flush(self):

@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 from tests import golden_data as gd  # noqa: E402
 
 
-def test_streaming_matches_direct():
+@pytest.mark.parametrize("zero_copy", [True, False])
+def test_streaming_matches_direct(zero_copy):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2604_02586_b200.engine import FrameEngine, StreamingEngine
@@ -25,7 +26,7 @@ def test_streaming_matches_direct():
         t = (target + np.array([shift, -0.5 * shift])).astype(np.float32)
         inputs.append((torch.from_numpy(g).pin_memory(), torch.from_numpy(t).pin_memory(),
                        torch.from_numpy(valid.astype(np.uint8)).pin_memory()))
-    streamer = StreamingEngine()
+    streamer = StreamingEngine(zero_copy_tracks=zero_copy)
     results = [StreamingEngine.result_buffer(len(g)) for _ in inputs]
     events = [streamer.step(gh, cams, th, vh, res) for (gh, th, vh), res in zip(inputs, results)]
     assert events[0] is None and all(e is not None for e in events[1:])
@@ -67,3 +68,43 @@ def test_trkf_batch_to_device(tmp_path):
     b = eng.compensate(t32, valid.astype(np.uint8))
     for k in ("delta_mean", "rotation", "scale", "status", "weight_sum", "pixel_count"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_zero_copy_tracks_bit_identical(dtype):
+    """Tracks in pinned host memory are read in place by K2 (zero-copy: only the occupied tiles'
+    quadrants cross PCIe): every output equals the run on device-resident copies bit for bit;
+    pageable host memory is refused by the C ABI (a kernel cannot read it) and copied by the
+    Python engine."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import ctypes
+
+    from paper_2604_02586_b200 import _native as nat
+    from paper_2604_02586_b200.engine import FrameEngine
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    t = np.ascontiguousarray(target.astype(dtype))
+    v = np.ascontiguousarray(valid.astype(np.uint8))
+    eng = FrameEngine().bin(d["gaussians"], d["cameras"])
+    dev = eng.compensate(torch.from_numpy(t).cuda(), torch.from_numpy(v).cuda())
+    th, vh = torch.from_numpy(t).pin_memory(), torch.from_numpy(v).pin_memory()
+    zc = eng.compensate(th, vh)
+    torch.cuda.synchronize()
+    keys = ("delta_mean", "rotation", "scale", "status", "motion_status", "motion_a", "motion_b",
+            "weight_sum", "pixel_count", "static_pixel_count", "static_weight_sum")
+    for k in keys:
+        assert torch.equal(getattr(zc, k), getattr(dev, k)), k
+    pageable = eng.compensate(torch.from_numpy(t), torch.from_numpy(v))  # copied to the device
+    for k in keys:
+        assert torch.equal(getattr(pageable, k), getattr(dev, k)), k
+    out = eng.alloc_outputs()
+    m = nat.Motions(0, 0, 0, 0, 0, 0, 0)
+    u = nat.Updates(nat.dptr(out.delta_mean).value, nat.dptr(out.rotation).value,
+                    nat.dptr(out.scale).value, nat.dptr(out.status).value)
+    rc = nat.lib().ts_frame_compensate(
+        eng.plan.handle, ctypes.c_void_p(t.ctypes.data),
+        nat.TS_TRACK_F32 if dtype == np.float32 else nat.TS_TRACK_F64,
+        ctypes.c_void_p(v.ctypes.data), ctypes.byref(m), ctypes.byref(u), None)
+    assert rc == nat.TS_E_INVALID_ARGUMENT
+    assert eng.occupied_tiles() > 0
