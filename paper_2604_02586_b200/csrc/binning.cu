@@ -141,19 +141,13 @@ __global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restri
   }
 }
 
-__global__ void k1_gather_counts(const uint32_t *__restrict__ val, const uint32_t *__restrict__ ntiles,
-                                 uint32_t *__restrict__ cnt_sorted, int64_t M) {
-  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < M) cnt_sorted[k] = ntiles[val[k]];
-}
-
 // One warp per 32 consecutive depth-sorted gvs: their instances are one contiguous run of the
 // output (exclusive scan of the counts), so the lanes write it cooperatively -- instance e of the
 // run belongs to the last lane whose offset is <= e (binary search over the 32 offsets) and is
 // its (k / width, k % width) tile, k = e - offset.  Coalesced stores and no per-lane loop over
 // large bounding boxes (a 200-tile Gaussian no longer idles 31 lanes).
 __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
-                                               const uint32_t *__restrict__ cnt_sorted,
+                                               const uint32_t *__restrict__ ntiles,
                                                const uint32_t *__restrict__ off_sorted,
                                                const RasterRec *__restrict__ rec, int64_t M,
                                                int tiles_x, uint32_t *__restrict__ tkey,
@@ -168,17 +162,17 @@ __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
   uint32_t c = 0, o;
   Owner me{0u, 0u, 0, 0, 1, 0};
   if (k < M) {
-    c = cnt_sorted[k];
+    me.gv = val[k];
+    c = ntiles[me.gv];
     o = off_sorted[k];
     if (c) {
-      me.gv = val[k];
       const RasterRec r = rec[me.gv];
       me.tx0 = (int16_t)(r.x0 / TS_TILE);
       me.ty0 = (int16_t)(r.y0 / TS_TILE);
       me.wt = (int16_t)(r.x1 / TS_TILE - me.tx0 + 1);
     }
   } else {
-    o = off_sorted[M - 1] + cnt_sorted[M - 1];  // past the end: offset = total
+    o = off_sorted[M - 1] + ntiles[val[M - 1]];  // past the end: offset = total
   }
   const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
   const uint32_t end = __shfl_sync(0xffffffffu, o + c, 31);
@@ -198,20 +192,35 @@ __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
   }
 }
 
+// [start, end) of every (view, tile) list.  After the stable tile sort the instances are ordered
+// by the composite c = tile_in_view * V + view (views in order inside a tile position, since
+// the emission is view-major), so one thread per (view, tile) binary-searches the first
+// instance with composite >= c and >= c + 1 (no pass over the instances).
+__device__ __forceinline__ uint32_t composite(const uint32_t *tkey, const uint32_t *tval,
+                                              int64_t i, double inv_n, uint32_t V) {
+  // view = floor((gv + 0.5) / n) in fp64 (exact: never within 2e-10 of an integer)
+  return tkey[i] * V + (uint32_t)(((double)tval[i] + 0.5) * inv_n);
+}
+
 __global__ void k1_tile_ranges(const uint32_t *__restrict__ tkey, const uint32_t *__restrict__ tval,
-                               int64_t n_inst, double inv_n, int tiles_per_view,
+                               int64_t n_inst, double inv_n, int V, int tiles_per_view,
                                uint32_t *__restrict__ range) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_inst) return;
-  // global tile id = view * tiles_per_view + tile-in-view, view = gv / n computed as
-  // floor((gv + 0.5) / n) in fp64 (exact: the quotient is never within 2e-10 of an integer)
-  auto gtile = [&](int64_t k) {
-    const uint32_t v = (uint32_t)(((double)tval[k] + 0.5) * inv_n);
-    return v * (uint32_t)tiles_per_view + tkey[k];
-  };
-  const uint32_t t = gtile(i);
-  if (i == 0 || gtile(i - 1) != t) range[2 * t] = (uint32_t)i;
-  if (i == n_inst - 1 || gtile(i + 1) != t) range[2 * t + 1] = (uint32_t)(i + 1);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // global tile v*tpv + t
+  if (g >= (int64_t)V * tiles_per_view) return;
+  const uint32_t v = (uint32_t)(g / tiles_per_view), t = (uint32_t)(g - (int64_t)v * tiles_per_view);
+  const uint32_t c = t * (uint32_t)V + v;
+  uint32_t out[2];
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    int64_t lo = 0, hi = n_inst;  // first index with composite >= c + e
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (composite(tkey, tval, mid, inv_n, (uint32_t)V) < c + (uint32_t)e) lo = mid + 1;
+      else hi = mid;
+    }
+    out[e] = (uint32_t)lo;
+  }
+  reinterpret_cast<uint2 *>(range)[g] = make_uint2(out[0], out[1]);
 }
 
 // _project_all for the stage API (one view).
@@ -260,22 +269,19 @@ void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth6
                         cudaStream_t s) {
   if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M);
 }
-void launch_k1_gather_counts(const uint32_t *val, const uint32_t *ntiles, uint32_t *cnt_sorted,
-                             int64_t M, cudaStream_t s) {
-  if (M) k1_gather_counts<<<blocks(M, 256), 256, 0, s>>>(val, ntiles, cnt_sorted, M);
-}
-void launch_k1_emit(const uint32_t *val, const uint32_t *cnt_sorted, const uint32_t *off_sorted,
+void launch_k1_emit(const uint32_t *val, const uint32_t *ntiles, const uint32_t *off_sorted,
                     const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
                     uint32_t *tkey, uint32_t *tval, cudaStream_t s) {
   if (M)
-    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, cnt_sorted, off_sorted, rec, M, tiles_x, tkey,
+    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, ntiles, off_sorted, rec, M, tiles_x, tkey,
                                            tval);
 }
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
-                           int tiles_per_view, uint32_t *range, cudaStream_t s) {
-  if (n_inst)
-    k1_tile_ranges<<<blocks(n_inst, 256), 256, 0, s>>>(tkey, tval, n_inst, 1.0 / (double)n,
-                                                       tiles_per_view, range);
+                           int V, int tiles_per_view, uint32_t *range, cudaStream_t s) {
+  const int64_t T = (int64_t)V * tiles_per_view;
+  if (T)
+    k1_tile_ranges<<<blocks(T, 256), 256, 0, s>>>(tkey, tval, n_inst, 1.0 / (double)n, V,
+                                                  tiles_per_view, range);
 }
 void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
                          double *depth, double *cov2, uint8_t *in_front, cudaStream_t s) {
