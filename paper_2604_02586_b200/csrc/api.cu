@@ -358,9 +358,8 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->tval2, 4 * (ni + 1));
   if (ni == 0) TS_CUDA_TRY(cudaMemsetAsync(p->range.p, 0, 8 * ntile_total, s));
   if (ni > 0) {
-    launch_k1_emit(ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->ntiles), ptr<uint32_t>(p->off_sorted),
-                   ptr<RasterRec>(p->rec), NV, n, p->tiles_x, p->tpv, ptr<uint32_t>(p->tkey),
-                   ptr<uint32_t>(p->tval), s);
+    launch_k1_emit(ptr<uint32_t>(p->dval2), ptr<int16_t>(p->bbox), ptr<uint32_t>(p->off_sorted),
+                   NV, p->tiles_x, ptr<uint32_t>(p->tkey), ptr<uint32_t>(p->tval), s);
     const int tbits = bits_for((uint64_t)p->tpv);  // tile within the view (see binning.cu)
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
       return k1_sort_pairs(tmp, bytes, ptr<uint32_t>(p->tkey), ptr<uint32_t>(p->tkey2),

@@ -146,11 +146,14 @@ __global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restri
 // run belongs to the last lane whose offset is <= e (binary search over the 32 offsets) and is
 // its (k / width, k % width) tile, k = e - offset.  Coalesced stores and no per-lane loop over
 // large bounding boxes (a 200-tile Gaussian no longer idles 31 lanes).
+// The owner's bbox comes from the 8-byte bbox array (one sector per random gv instead of the
+// record's line plus a separate count gather); its tile count is derived from it (the sentinel
+// bbox {0, -1, 0, -1} of a non-binned gv gives 0 with arithmetic shifts).
 __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
-                                               const uint32_t *__restrict__ ntiles,
+                                               const int16_t *__restrict__ bbox,
                                                const uint32_t *__restrict__ off_sorted,
-                                               const RasterRec *__restrict__ rec, int64_t M,
-                                               int tiles_x, uint32_t *__restrict__ tkey,
+                                               int64_t M, int tiles_x,
+                                               uint32_t *__restrict__ tkey,
                                                uint32_t *__restrict__ tval) {
   struct Owner {
     uint32_t off, gv;
@@ -163,16 +166,17 @@ __global__ void __launch_bounds__(256) k1_emit(const uint32_t *__restrict__ val,
   Owner me{0u, 0u, 0, 0, 1, 0};
   if (k < M) {
     me.gv = val[k];
-    c = ntiles[me.gv];
+    const short4 bb = reinterpret_cast<const short4 *>(bbox)[me.gv];  // x0 x1 y0 y1
     o = off_sorted[k];
-    if (c) {
-      const RasterRec r = rec[me.gv];
-      me.tx0 = (int16_t)(r.x0 / TS_TILE);
-      me.ty0 = (int16_t)(r.y0 / TS_TILE);
-      me.wt = (int16_t)(r.x1 / TS_TILE - me.tx0 + 1);
-    }
+    const int tx0 = bb.x >> 4, ty0 = bb.z >> 4, wt = (bb.y >> 4) - tx0 + 1;
+    c = (uint32_t)(wt * ((bb.w >> 4) - ty0 + 1));
+    me.tx0 = (int16_t)tx0;
+    me.ty0 = (int16_t)ty0;
+    me.wt = (int16_t)(c ? wt : 1);
   } else {
-    o = off_sorted[M - 1] + ntiles[val[M - 1]];  // past the end: offset = total
+    const short4 bb = reinterpret_cast<const short4 *>(bbox)[val[M - 1]];
+    o = off_sorted[M - 1] +  // past the end: offset = total
+        (uint32_t)(((bb.y >> 4) - (bb.x >> 4) + 1) * ((bb.w >> 4) - (bb.z >> 4) + 1));
   }
   const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
   const uint32_t end = __shfl_sync(0xffffffffu, o + c, 31);
@@ -269,12 +273,10 @@ void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth6
                         cudaStream_t s) {
   if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M);
 }
-void launch_k1_emit(const uint32_t *val, const uint32_t *ntiles, const uint32_t *off_sorted,
-                    const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
-                    uint32_t *tkey, uint32_t *tval, cudaStream_t s) {
-  if (M)
-    k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, ntiles, off_sorted, rec, M, tiles_x, tkey,
-                                           tval);
+void launch_k1_emit(const uint32_t *val, const int16_t *bbox, const uint32_t *off_sorted,
+                    int64_t M, int tiles_x, uint32_t *tkey, uint32_t *tval, cudaStream_t s) {
+  static_assert(TS_TILE == 16, "k1_emit derives tiles with >> 4");
+  if (M) k1_emit<<<blocks(M, 256), 256, 0, s>>>(val, bbox, off_sorted, M, tiles_x, tkey, tval);
 }
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
                            int V, int tiles_per_view, uint32_t *range, cudaStream_t s) {

@@ -12,9 +12,8 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
                        uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s);
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         cudaStream_t s);
-void launch_k1_emit(const uint32_t *val, const uint32_t *ntiles, const uint32_t *off_sorted,
-                    const RasterRec *rec, int64_t M, int64_t n, int tiles_x, int tiles_per_view,
-                    uint32_t *tkey, uint32_t *tval, cudaStream_t s);
+void launch_k1_emit(const uint32_t *val, const int16_t *bbox, const uint32_t *off_sorted,
+                    int64_t M, int tiles_x, uint32_t *tkey, uint32_t *tval, cudaStream_t s);
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
                            int V, int tiles_per_view, uint32_t *range, cudaStream_t s);
 void launch_project_view(const double *G, int64_t n, const ts_camera &cam, double *mean2,
