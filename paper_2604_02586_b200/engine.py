@@ -200,39 +200,51 @@ class FrameEngine:
 
 
 class StreamingEngine:
-    """Double-buffered end-to-end driver: pinned host inputs in, pinned host results out.
+    """Pipelined end-to-end driver: pinned host inputs in, pinned host results out.
 
-    Three streams: H2D copies, compute, D2H copies.  `step(inputs_k)` enqueues the H2D copy of
-    step k's Gaussians and then the compute of the PREVIOUS step (k-1), so the copy of step k is
-    already queued when step k-1's binning briefly synchronises the host (the instance count);
-    the D2H of a step's results runs on its own stream from one of two output buffers, so the
-    compute stream moves on to the next frame at once.  Tracks given as pinned host tensors are
-    not copied at all (`zero_copy_tracks=True`, the default): K2 reads the 8x8 quadrants of the
-    occupied tiles in place over PCIe, one work unit ahead (about a tenth of the track bytes at
-    the benchmark configs); with `zero_copy_tracks=False` the whole arrays are copied on the H2D
-    stream.  Input slots and output buffers are reused in turn,
-    ordered with CUDA events.  `step` returns the event after which the previous step's results
-    are in its host buffer (None for the first call); `flush()` runs the last pending step.  The
-    caller must leave step k's host inputs unchanged until the event returned by the call that
-    computes step k has completed.
+    Streams: one H2D stream, two compute streams and one D2H stream.  `step(inputs_k)` enqueues
+    the H2D copy of step k's inputs and then the compute of the PREVIOUS step (k-1), so the copy
+    of step k is already queued when step k-1's binning briefly synchronises the host (the
+    instance count).  Consecutive steps compute on alternating engines (binning plans) and
+    compute streams, so two frames are in flight: one frame's binning fills the SMs that the
+    other's latency-bound K3/K4 leave idle.  The D2H of a step's results runs on its own stream
+    from that engine's output buffer.  Tracks given as pinned host tensors are not copied at all
+    (`zero_copy_tracks=True`, the default): K2 reads the 8x8 quadrants of the occupied tiles in
+    place over PCIe (about a tenth of the track bytes at the benchmark configs); with
+    `zero_copy_tracks=False` the whole arrays are copied on the H2D stream.  Input slots and
+    output buffers are reused in turn, ordered with CUDA events.  `step` returns the event after
+    which the previous step's results are in its host buffer (None for the first call);
+    `flush()` runs the last pending step; `wait_all(stream)` orders `stream` after every result
+    copy issued so far.  The caller must leave step k's host inputs unchanged until the event
+    returned by the call that computes step k has completed.
     """
 
-    N_SLOTS = 3  # input slots: the copy of step k+1 never waits for step k-1's compute
+    N_SLOTS = 4  # input slots: the copy of step k+1 never waits for steps k-1 / k-2
+    N_ENGINES = 2  # frames in flight
 
     def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks: bool = True):
         torch = _torch()
-        self.eng = engine if engine is not None else FrameEngine()
+        self.engines = [engine if engine is not None else FrameEngine()] + \
+            [FrameEngine() for _ in range(self.N_ENGINES - 1)]
         self.zero_copy_tracks = zero_copy_tracks
         self.copy_stream = torch.cuda.Stream()
-        self.comp_stream = torch.cuda.Stream()
+        self.comp_streams = [torch.cuda.Stream() for _ in range(self.N_ENGINES)]
         self.d2h_stream = torch.cuda.Stream()
         self._slots = [None] * self.N_SLOTS
         self._free = [None] * self.N_SLOTS  # input slot i reusable after this compute event
-        self._outs = [None, None]
-        self._out_free = [None, None]  # output buffer j reusable after this D2H event
+        self._outs = [None] * self.N_ENGINES
+        self._out_free = [None] * self.N_ENGINES  # engine e's outputs reusable after this D2H
         self._k = 0
-        self._j = 0
+        self._c = 0
         self._pending = None
+
+    @property
+    def eng(self):
+        return self.engines[0]
+
+    @property
+    def comp_stream(self):
+        return self.comp_streams[0]
 
     def _slot(self, i, g_host, t_host, v_host, tracks):
         torch = _torch()
@@ -255,16 +267,16 @@ class StreamingEngine:
 
     def _compute(self, pending):
         torch = _torch()
-        i, g_d, t_d, v_d, staged, ready, cameras, res_host, config = pending
-        j = self._j
-        self._j ^= 1
-        cs = self.comp_stream
+        i, g_d, t_d, v_d, ready, cameras, res_host, config = pending
+        e = self._c % self.N_ENGINES
+        self._c += 1
+        eng, cs = self.engines[e], self.comp_streams[e]
         cs.wait_event(ready)
-        if self._out_free[j] is not None:
-            cs.wait_event(self._out_free[j])
-        self.eng.bin(g_d, cameras, config, stream=cs)
-        out = self.eng.compensate(t_d, v_d, self._outs[j], stream=cs)
-        self._outs[j] = out
+        if self._out_free[e] is not None:
+            cs.wait_event(self._out_free[e])
+        eng.bin(g_d, cameras, config, stream=cs)
+        out = eng.compensate(t_d, v_d, self._outs[e], stream=cs)
+        self._outs[e] = out
         with torch.cuda.stream(cs):
             res = torch.cat([out.delta_mean, out.rotation, out.scale,
                              out.status.to(torch.float64)[:, None]], 1)
@@ -278,7 +290,7 @@ class StreamingEngine:
             res_host.copy_(res, non_blocking=True)
             done = torch.cuda.Event()
             done.record(ds)
-        self._out_free[j] = done
+        self._out_free[e] = done
         self.out = out
         return done
 
@@ -287,24 +299,29 @@ class StreamingEngine:
         torch = _torch()
         i = self._k % self.N_SLOTS
         self._k += 1
-        staged = self.zero_copy_tracks and _pinned_pair(t_host, v_host)
-        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host, not staged)
+        zero_copy = self.zero_copy_tracks and _pinned_pair(t_host, v_host)
+        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host, not zero_copy)
         with torch.cuda.stream(self.copy_stream):
             if self._free[i] is not None:
                 self.copy_stream.wait_event(self._free[i])
             g_d.copy_(g_host, non_blocking=True)
-            if staged:
+            if zero_copy:
                 t_d, v_d = t_host, v_host  # read in place by K2
             else:
                 t_d.copy_(t_host, non_blocking=True)
                 v_d.copy_(v_host, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self.copy_stream)
-        prev, self._pending = self._pending, (i, g_d, t_d, v_d, staged, ready, cameras, res_host,
-                                              config)
+        prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config)
         return self._compute(prev) if prev is not None else None
 
     def flush(self):
         """Compute the last pending step; returns its results-ready event (or None)."""
         prev, self._pending = self._pending, None
         return self._compute(prev) if prev is not None else None
+
+    def wait_all(self, stream):
+        """Make `stream` wait for every result copy issued so far."""
+        for ev in self._out_free:
+            if ev is not None:
+                stream.wait_event(ev)
