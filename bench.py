@@ -388,10 +388,13 @@ def run_ours(args):
         bk2 = k2_bytes(n, nv, w, h)
         achieved = bk2 / (k2_ms / 1e3) / 1e9
         traffic = None
+        k2_instr = None
         tp = os.path.join(ROOT, "profiles", f"k2_traffic_{args.config}.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            traffic = tj.get("dram_bytes_per_launch")
+            k2_instr = tj.get("executed_warp_instructions_per_launch")
         stage_ms = {k: round(v[0] / max(v[1], 1), 4) for k, v in stages.items()}
         tallies = out.tallies()
         cpu = None
@@ -425,6 +428,13 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k2_raster_accumulate", "algorithmic_bytes": bk2,
                          "kernel_ms": k2_ms, "peak_kind": peak_kind},
+            # K2 is issue-bound, not HBM-bound: its executed warp instructions (committed ncu
+            # capture) over its live CUDA-event time vs 4 issue slots/clock on 148 SMs
+            "issue_roofline": None if k2_instr is None else {
+                "kernel": "k2_raster_accumulate", "achieved": k2_instr / (k2_ms / 1e3),
+                "peak": 4 * 148 * 1965e6, "unit": "warp-instructions/s",
+                "frac": k2_instr / (k2_ms / 1e3) / (4 * 148 * 1965e6),
+                "instructions_per_launch": k2_instr},
             "stage_ms": stage_ms, "tallies": tallies,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clk.summary(),

@@ -68,7 +68,7 @@ struct ts_plan {
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
       reg_static, reg_source, reg_euler, k4_ws, drange, k2_sched;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
-  int64_t n = 0, n_inst = 0, emit_n = 0, n_deg = 0;
+  int64_t n = 0, n_inst = 0, n_slots = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
   const double *gaussians = nullptr;
   std::vector<ts_camera> host_cams;
@@ -174,11 +174,29 @@ __global__ void k_fetch_contribs(const uint64_t *key_sorted, const uint32_t *idx
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-struct GatherCount {  // tile count of a (sorted) gv
-  const uint32_t *ntiles;
-  __host__ __device__ __forceinline__ uint32_t operator()(uint32_t gv) const {
+struct GatherCount {  // tile count of the i-th depth-sorted gv (0 at i == NV: scan total)
+  const uint32_t *sorted_gv, *ntiles;
+  int64_t nv;
+  __host__ __device__ __forceinline__ uint32_t operator()(int64_t i) const {
 #ifdef __CUDA_ARCH__
-    return ntiles[gv];
+    return i < nv ? ntiles[sorted_gv[i]] : 0u;
+#else
+    return 0u;
+#endif
+  }
+};
+
+// Partial-moment slots of gv i: one per 8x8 quadrant its bbox touches (only those can receive
+// a contribution); 0 for a non-binned gv (sentinel bbox {0, -1, 0, -1}) and for i == NV, so an
+// exclusive scan over NV + 1 entries ends with the total.
+struct QuadCount {
+  const int16_t *bbox;
+  int64_t nv;
+  __host__ __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+#ifdef __CUDA_ARCH__
+    if (i >= nv) return 0u;
+    const short4 bb = reinterpret_cast<const short4 *>(bbox)[i];
+    return (uint32_t)(((bb.y >> 3) - (bb.x >> 3) + 1) * ((bb.w >> 3) - (bb.z >> 3) + 1));
 #else
     return 0u;
 #endif
@@ -300,8 +318,8 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->ntiles, 4 * NV);
   ENSURE(p->status, NV);
   ENSURE(p->bbox, 8 * NV);
-  ENSURE(p->off_sorted, 4 * NV);
-  ENSURE(p->inst_base, 4 * NV);
+  ENSURE(p->off_sorted, 4 * (NV + 1));
+  ENSURE(p->inst_base, 4 * (NV + 1));
   const int64_t ntile_total = (int64_t)p->tpv * V;
   ENSURE(p->range, 8 * ntile_total);
   ENSURE(p->items, 4 * (ntile_total + 1));
@@ -327,26 +345,31 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
                        s);
     // instance offsets in depth order: scan of the tile counts gathered through the sorted gvs
     // (the gather is fused into the scan's loads)
-    GatherCount gc{ptr<uint32_t>(p->ntiles)};
-    cub::TransformInputIterator<uint32_t, GatherCount, const uint32_t *> cnt_it(
-        ptr<uint32_t>(p->dval2), gc);
+    cub::TransformInputIterator<uint32_t, GatherCount, cub::CountingInputIterator<int64_t>>
+        cnt_it(cub::CountingInputIterator<int64_t>(0),
+               GatherCount{ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->ntiles), NV});
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
       return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt_it, ptr<uint32_t>(p->off_sorted),
-                                           (int)NV, s);
+                                           (int)(NV + 1), s);
     }));
+    // partial-moment slot base of every gv (gv order): one slot per bbox quadrant
+    cub::TransformInputIterator<uint32_t, QuadCount, cub::CountingInputIterator<int64_t>> q_it(
+        cub::CountingInputIterator<int64_t>(0), QuadCount{ptr<int16_t>(p->bbox), NV});
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
-      return cub::DeviceScan::ExclusiveSum(tmp, bytes, ptr<uint32_t>(p->ntiles),
-                                           ptr<uint32_t>(p->inst_base), (int)NV, s);
+      return cub::DeviceScan::ExclusiveSum(tmp, bytes, q_it, ptr<uint32_t>(p->inst_base),
+                                           (int)(NV + 1), s);
     }));
-    // instance total (order-free) from the gv-order scan
-    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, ptr<uint32_t>(p->inst_base) + (NV - 1), 4,
+    // instance and slot totals (the scans' last entries)
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small, ptr<uint32_t>(p->off_sorted) + NV, 4,
                                 cudaMemcpyDeviceToHost, s));
-    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 1, ptr<uint32_t>(p->ntiles) + (NV - 1), 4,
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 1, ptr<uint32_t>(p->inst_base) + NV, 4,
                                 cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
-    p->n_inst = (int64_t)p->host_small[0] + (int64_t)p->host_small[1];
+    p->n_inst = (int64_t)p->host_small[0];
+    p->n_slots = (int64_t)p->host_small[1];
   } else {
     p->n_inst = 0;
+    p->n_slots = 0;
   }
   p->mark_end(ST_DEPTH_SORT, e1, s);
 
@@ -510,8 +533,9 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
     if (rc) return rc;
     if (kt != kv) return TS_E_INVALID_ARGUMENT;  // both on the device or both pinned host
   }
-  ENSURE(p->partial, sizeof(Partial) * TS_K2_SUBS * (ni + 1));
-  ENSURE(p->flag, TS_K2_SUBS * (ni + 1));
+  const int64_t ns = p->n_slots;  // one partial slot per (gv, bbox quadrant)
+  ENSURE(p->partial, sizeof(Partial) * (ns + 1));
+  ENSURE(p->flag, ns + 8);  // K3 reads the flags as aligned 32-bit words
   ts_motions m = motions ? *motions : ts_motions{};
   ts_motions im;
   {
@@ -532,7 +556,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
 
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
   cudaEvent_t e3 = p->mark_begin(s);
-  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, TS_K2_SUBS * (ni + 1), s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
   TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
                         ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,

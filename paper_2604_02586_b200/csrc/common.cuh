@@ -21,7 +21,6 @@
 #define TS_DET_FLOOR 1e-12    // splat.py:20
 #define TS_SIGMA_RADIUS 3.0   // splat.py:21
 #define TS_TILE 16            // tile edge in pixels (binning unit of K1/K2)
-#define TS_K2_SUBS 4          // partial sub-slots per (tile, Gaussian): K2 works on 8x8 quadrants
 #define TS_SINGULAR_GAP_REL 1e-9  // multiview.py:28
 
 #define TS_CUDA_TRY(expr)                       \

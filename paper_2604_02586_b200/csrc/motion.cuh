@@ -106,23 +106,29 @@ TS_HD void add_slot(const Partial *partial, uint32_t slot, double (&mom)[TS_NMOM
   scnt += (uint32_t)(counts >> 32);
 }
 
-// Add the flagged sub-slots of instances [i_begin, i_end) (step `stride`) of one gv, in order.
-// base4 = 4 * first instance; one 32-bit flag word per instance holds its four quadrant flags;
-// four words per round keep independent loads in flight for large bboxes.
-TS_HD void accumulate_slots(const Partial *partial, const uint8_t *flag, uint32_t base4,
-                            uint32_t i_begin, uint32_t i_end, uint32_t stride,
+// Add the flagged slots in [sb, se) of one gv (one slot per 8x8 quadrant of its bbox), in slot
+// order.  The flag bytes are read as aligned 32-bit words (4 slots each), four words per round
+// in flight; bytes outside [sb, se) are masked.  A warp can split the words: lane `first` of
+// `stride` takes words first, first + stride, ... (the flag array is padded past the end).
+TS_HD void accumulate_slots(const Partial *partial, const uint8_t *flag, uint32_t sb,
+                            uint32_t se, uint32_t first, uint32_t stride,
                             double (&mom)[TS_NMOM], uint32_t &cnt, uint32_t &scnt) {
-  static_assert(TS_K2_SUBS == 4, "flag words assume four sub-slots per instance");
-  for (uint32_t i0 = i_begin; i0 < i_end; i0 += 4 * stride) {
+  const uint32_t w_end = (se + 3) >> 2;
+  const uint32_t *fwords = reinterpret_cast<const uint32_t *>(flag);
+  for (uint32_t w0 = (sb >> 2) + first; w0 < w_end; w0 += 4 * stride) {
     uint32_t fw[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const uint32_t inst = i0 + q * stride;
-      fw[q] = inst < i_end ? *reinterpret_cast<const uint32_t *>(flag + base4 + 4 * inst) : 0u;
+      const uint32_t w = w0 + q * stride;
+      uint32_t f = w < w_end ? fwords[w] : 0u;
+      const uint32_t lo = sb > 4 * w ? sb - 4 * w : 0u;       // first byte inside the range
+      const uint32_t hi = se < 4 * w + 4 ? se - 4 * w : 4u;    // one past the last
+      const uint64_t keep = ((1ull << (8 * hi)) - 1ull) & ~((1ull << (8 * lo)) - 1ull);
+      fw[q] = f & (uint32_t)keep;
     }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const uint32_t slot0 = base4 + 4 * (i0 + q * stride);
+      const uint32_t slot0 = 4 * (w0 + q * stride);
       uint32_t f4 = fw[q];
       while (f4) {
         const int sub = (ffs_hd(f4) - 1) >> 3;
@@ -167,14 +173,14 @@ TS_HD GvMotion solve_moments(const double (&mom)[TS_NMOM], uint32_t cnt, uint32_
 }
 
 // Sum the (instance, quadrant) sub-slots of one gv in fixed order and fit its affine motion.
-TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t base4,
+TS_HD GvMotion solve_gv(const Partial *partial, const uint8_t *flag, uint32_t sb,
                         uint32_t nslots, int anchor_x, int anchor_y, double det_floor,
                         int min_pixels, double min_weight) {
   double mom[TS_NMOM];
 #pragma unroll
   for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
   uint32_t cnt = 0, scnt = 0;
-  accumulate_slots(partial, flag, base4, 0, nslots / 4, 1, mom, cnt, scnt);
+  accumulate_slots(partial, flag, sb, sb + nslots, 0, 1, mom, cnt, scnt);
   return solve_moments(mom, cnt, scnt, anchor_x, anchor_y, det_floor, min_pixels, min_weight);
 }
 

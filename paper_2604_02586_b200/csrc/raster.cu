@@ -44,7 +44,7 @@ struct K2Params {
   const RasterRec *rec;
   const uint32_t *inst_gv;     // sorted instances: gv
   const uint32_t *tile_range;  // [start, end) per global tile
-  const uint32_t *inst_base;   // per gv: first instance slot (gv-order scan of tile counts)
+  const uint32_t *inst_base;   // per gv: first partial slot (gv-order scan of bbox quadrant counts)
   const uint32_t *items;       // non-empty global tile ids
   const uint32_t *n_items;     // device count of items
   uint32_t *work_counter;      // zeroed before launch
@@ -53,7 +53,7 @@ struct K2Params {
   int W, H, tiles_x, tiles_per_view;
   double alpha_cutoff, early_stop, static_thr;
   // accumulate mode
-  Partial *partial;  // 4 sub-slots (quadrants) per instance
+  Partial *partial;  // one slot per (gv, 8x8 quadrant of its bbox)
   uint8_t *flag;
   // emit mode
   unsigned long long *emit_count;
@@ -296,9 +296,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
           S.rec[lane] = r;
           S.rect[lane] = rect;
           if (MODE == K2_ACCUMULATE) {
-            const int tx0 = r.x0 / TS_TILE, tx1 = r.x1 / TS_TILE, ty0 = r.y0 / TS_TILE;
-            S.slot[lane] = 4u * (P.inst_base[gv] + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) +
-                                                             (tx - tx0))) + (uint32_t)quad;
+            // one slot per 8x8 quadrant of the gv's bbox, row-major from its top-left quadrant
+            const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
+            S.slot[lane] = P.inst_base[gv] + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
+                                                        ((qx0 >> 3) - bx0));
             S.anc[lane] = make_int2(anchor_x(r), anchor_y(r));
           } else {
             S.slot[lane] = gv;

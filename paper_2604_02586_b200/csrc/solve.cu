@@ -25,8 +25,8 @@ __device__ __forceinline__ bool finite6(const double *x) {
   return ok;
 }
 
-// A gv with more instances than this is summed by its whole warp (k3_solve).
-constexpr uint32_t K3_BIG = 8;
+// A gv with more partial slots than this is summed by its whole warp (k3_solve).
+constexpr uint32_t K3_BIG = 32;
 
 __device__ __forceinline__ void store_motion(ts_motions m, int64_t gv, const GvMotion &r) {
   m.status[gv] = r.status;
@@ -52,35 +52,37 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial 
   const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool valid = gv < NV;
-  const uint32_t nt = valid ? ntiles[gv] : 0u;
-  // gvs with many instances (large bboxes) are summed by the whole warp afterwards, so one
-  // straggler no longer holds its 31 neighbours (lane i takes instances i, i+32, ...; the lanes
+  // one partial slot per 8x8 quadrant of the gv's bbox (0 for the sentinel bbox of a non-binned
+  // gv), starting at inst_base[gv]
+  const short4 bb = valid ? reinterpret_cast<const short4 *>(bbox)[gv] : make_short4(0, -1, 0, -1);
+  const uint32_t nq = (uint32_t)(((bb.y >> 3) - (bb.x >> 3) + 1) * ((bb.w >> 3) - (bb.z >> 3) + 1));
+  // gvs with many slots (large bboxes) are summed by the whole warp afterwards, so one
+  // straggler no longer holds its 31 neighbours (lane i takes flag words i, i+32, ...; the lanes
   // then combine in a fixed xor tree: deterministic)
-  const bool big = nt > K3_BIG;
-  uint32_t base4 = 0;
+  const bool big = nq > K3_BIG;
+  uint32_t sb = 0;
   int ax = 0, ay = 0;
-  if (nt) {
-    const short4 bb = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
-    base4 = TS_K2_SUBS * inst_base[gv];
+  if (nq) {
+    sb = inst_base[gv];
     ax = ((int)bb.x + (int)bb.y) >> 1;
     ay = ((int)bb.z + (int)bb.w) >> 1;
   }
   if (valid && !big) {
-    const GvMotion r = solve_gv(partial, flag, base4, TS_K2_SUBS * nt, ax, ay, det_floor,
-                                min_pixels, min_weight);
+    const GvMotion r = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels,
+                                min_weight);
     store_motion(m, gv, r);
   }
   uint32_t bigmask = __ballot_sync(0xffffffffu, valid && big);
   while (bigmask) {
     const int j = __ffs(bigmask) - 1;
     bigmask &= bigmask - 1;
-    const uint32_t ntj = __shfl_sync(0xffffffffu, nt, j);
-    const uint32_t b4j = __shfl_sync(0xffffffffu, base4, j);
+    const uint32_t nqj = __shfl_sync(0xffffffffu, nq, j);
+    const uint32_t sbj = __shfl_sync(0xffffffffu, sb, j);
     double mom[TS_NMOM];
 #pragma unroll
     for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
     uint32_t cnt = 0, scnt = 0;
-    accumulate_slots(partial, flag, b4j, lane, ntj, 32, mom, cnt, scnt);
+    accumulate_slots(partial, flag, sbj, sbj + nqj, lane, 32, mom, cnt, scnt);
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
