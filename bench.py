@@ -299,6 +299,7 @@ def run_ours(args):
             if world > 1:
                 stream.wait_stream(streams[i])
                 dist.gather(updated_rows(outs[i]), gather_buf if rank == 0 else None, dst=0)
+                streams[i].wait_stream(stream)  # step k+2 rewrites outs[i] after this read
             torch.cuda.nvtx.range_pop()
         for s_ in streams:
             stream.wait_stream(s_)
@@ -317,8 +318,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     stages = eng.plan.timing_read()
     eng.plan.timing(False)
-    # free the second engine before the e2e runs (its partial-moment workspace is 512 B per tile
-    # instance: 56 GB at cfg5)
+    # free the second engine before the e2e runs (its partial-moment workspace is 128 B per bbox
+    # quadrant: 27 GB at cfg5)
     engs[1].plan.close()
     del engs, outs, streams
     torch.cuda.empty_cache()
