@@ -524,7 +524,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
   const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
   // tracks: device memory, or pinned host memory that K2 reads in place (zero-copy: only the
-  // 8x8 quadrants of occupied tiles cross PCIe, prefetched one work unit ahead)
+  // 8x8 quadrants of occupied tiles cross PCIe)
   {
     int kt = 0, kv = 0;
     int rc = device_view(track_target, &track_target, &kt);
