@@ -112,11 +112,10 @@ int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_cam
 
 /* K2 fused raster-accumulate -> K3 per-view affine solve -> K4 multi-view fuse for one target
  * frame.  track_target: (V, H, W, 2) of TS_TRACK_F32/F64; track_valid: (V, H, W) uint8.
- * The track arrays are both device memory, or both page-locked (pinned) host memory: K2 then
- * reads only the 8x8 quadrants of occupied tiles in place over PCIe (zero-copy), about a tenth
- * of the track bytes at the benchmark configs; the host must
- * not modify them until the frame's work on `stream` completes.  Pageable host memory, or one
- * array on each side: TS_E_INVALID_ARGUMENT.
+ * Each track array is device memory or page-locked (pinned) host memory: K2 reads the pinned
+ * host arrays in place over PCIe (zero-copy), only the 8x8 quadrants of occupied tiles -- about
+ * a tenth of the pixels at the benchmark configs; the host must not modify them until the
+ * frame's work on `stream` completes.  Pageable host memory: TS_E_INVALID_ARGUMENT.
  * motions may have NULL members (then only the internal copy is kept); updates must be valid. */
 int ts_frame_compensate(ts_plan *plan, const void *track_target, int32_t track_dtype,
                         const uint8_t *track_valid, const ts_motions *motions,

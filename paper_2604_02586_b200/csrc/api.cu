@@ -531,7 +531,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
     if (rc) return rc;
     rc = device_view(track_valid, reinterpret_cast<const void **>(&track_valid), &kv);
     if (rc) return rc;
-    if (kt != kv) return TS_E_INVALID_ARGUMENT;  // both on the device or both pinned host
+    (void)kt;  // each array on the device or in pinned host memory
+    (void)kv;
   }
   const int64_t ns = p->n_slots;  // one partial slot per (gv, bbox quadrant)
   ENSURE(p->partial, sizeof(Partial) * (ns + 1));

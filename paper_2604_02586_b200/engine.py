@@ -32,13 +32,15 @@ def _torch():
     return torch
 
 
-def _pinned_pair(tgt, val):
-    """True for contiguous page-locked CPU tensors, which kernels may read in place."""
+def _pinned(t):
+    """True for a contiguous page-locked CPU tensor, which kernels may read in place."""
     torch = _torch()
-    return (isinstance(tgt, torch.Tensor) and isinstance(val, torch.Tensor)
-            and tgt.device.type == "cpu" and val.device.type == "cpu"
-            and tgt.is_contiguous() and val.is_contiguous()
-            and tgt.is_pinned() and val.is_pinned())
+    return (isinstance(t, torch.Tensor) and t.device.type == "cpu" and t.is_contiguous()
+            and t.is_pinned())
+
+
+def _pinned_pair(tgt, val):
+    return _pinned(tgt) and _pinned(val)
 
 
 def as_device(x, dtype, device=None):
@@ -156,18 +158,22 @@ class FrameEngine:
         if self._gauss is None:
             raise RuntimeError("FrameEngine.bin() must run before compensate()")
         tgt, val = track_target, track_valid
-        if _pinned_pair(tgt, val):
-            # zero-copy: K2 reads the occupied tiles' quadrants in place (C ABI)
-            if tgt.dtype not in (torch.float32, torch.float64) or val.dtype != torch.uint8:
-                raise TypeError("pinned tracks must be float32/float64 targets and uint8 valid")
+        # each array: a CUDA tensor as is; a pinned CPU tensor is read in place by K2 (zero-copy:
+        # only the occupied tiles' quadrants cross PCIe); anything else is copied to the device
+        if _pinned(tgt):
+            if tgt.dtype not in (torch.float32, torch.float64):
+                raise TypeError("pinned track targets must be float32 or float64")
         elif not isinstance(tgt, torch.Tensor):
             tgt = np.asarray(tgt)
             tgt = as_device(tgt, torch.float32 if tgt.dtype == np.float32 else torch.float64)
-            val = as_device(val, torch.uint8)
         else:
             tgt = tgt.contiguous()
             if tgt.device.type != "cuda":
                 tgt = as_device(tgt, tgt.dtype)
+        if _pinned(val):
+            if val.dtype != torch.uint8:
+                raise TypeError("pinned track validity must be uint8")
+        else:
             val = as_device(val, torch.uint8)
         expect = (self.n_views, self.height, self.width)
         if tuple(tgt.shape) != expect + (2,) or tuple(val.shape) != expect:

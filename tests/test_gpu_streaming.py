@@ -95,6 +95,9 @@ def test_zero_copy_tracks_bit_identical(dtype):
             "weight_sum", "pixel_count", "static_pixel_count", "static_weight_sum")
     for k in keys:
         assert torch.equal(getattr(zc, k), getattr(dev, k)), k
+    mixed = eng.compensate(th, torch.from_numpy(v).cuda())  # targets in place, valid on device
+    for k in keys:
+        assert torch.equal(getattr(mixed, k), getattr(dev, k)), k
     pageable = eng.compensate(torch.from_numpy(t), torch.from_numpy(v))  # copied to the device
     for k in keys:
         assert torch.equal(getattr(pageable, k), getattr(dev, k)), k
