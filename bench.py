@@ -354,6 +354,7 @@ def run_ours(args):
         streamer.copy_stream.wait_event(e0)  # no copy of the timed steps starts before e0
         for cs in streamer.comp_streams[1:]:
             cs.wait_event(e0)
+        streamer.steps_zero_copy = streamer.steps_full_copy = 0
         for k in range(args.steps):
             streamer.step(g_host, cams, t_hosts[k & 1], v_hosts[k & 1], res_host)
         streamer.flush()  # the K-th step's compute (each step computes its predecessor)
@@ -367,19 +368,24 @@ def run_ours(args):
             t = torch.tensor([ms_], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_ = float(t.item())
-        return ms_
+        return ms_, streamer.steps_zero_copy, streamer.steps_full_copy
 
-    ms_e2e_copy = time_e2e(False)
     import gc
-    gc.collect()  # the first streamer's second engine
+    ms_e2e_copy = time_e2e(False)[0]
+    gc.collect()  # the previous streamer's second engine
     torch.cuda.empty_cache()
-    ms_e2e = time_e2e(True)
+    ms_e2e_zc = time_e2e(True)[0]
+    gc.collect()
+    torch.cuda.empty_cache()
+    # the StreamingEngine default: per-step choice between the two
+    ms_e2e, n_zc, n_fc = time_e2e("auto")
     occupied = eng.occupied_tiles()
     track_px_bytes = 2 * t_hosts[0].element_size() + 1
     h2d_copy = g_host.numel() * 8 + t_hosts[0].numel() * t_hosts[0].element_size() + \
         v_hosts[0].numel()
     # zero-copy: Gaussians + the 256 pixels of every occupied tile (edge tiles: upper bound)
-    h2d = g_host.numel() * 8 + occupied * 256 * track_px_bytes
+    h2d_zc = g_host.numel() * 8 + occupied * 256 * track_px_bytes
+    h2d = (n_zc * h2d_zc + n_fc * h2d_copy) / max(n_zc + n_fc, 1)  # the auto run's steps
     d2h = res_host.numel() * 8
 
     line = None
@@ -422,6 +428,11 @@ def run_ours(args):
                     "ms_per_step": ms_e2e,
                     "tracks": f"zero-copy: K2 reads the {occupied} occupied 16x16 tiles in place "
                               f"from pinned host memory (two host track sets alternate)",
+                    "mode": f"auto: copies the whole track arrays when that copy fits under "
+                            f"the compute, reads the occupied tiles in place otherwise "
+                            f"({n_zc} steps in place, {n_fc} copied)",
+                    "zero_copy": {"value": n * nv * world / (ms_e2e_zc / 1e3),
+                                  "ms_per_step": ms_e2e_zc, "h2d_bytes_per_step": int(h2d_zc)},
                     "full_copy": {"value": n * nv * world / (ms_e2e_copy / 1e3),
                                   "ms_per_step": ms_e2e_copy,
                                   "h2d_bytes_per_step": int(h2d_copy)}},

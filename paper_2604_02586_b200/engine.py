@@ -214,10 +214,14 @@ class StreamingEngine:
     instance count).  Consecutive steps compute on alternating engines (binning plans) and
     compute streams, so two frames are in flight: one frame's binning fills the SMs that the
     other's latency-bound K3/K4 leave idle.  The D2H of a step's results runs on its own stream
-    from that engine's output buffer.  Tracks given as pinned host tensors are not copied at all
-    (`zero_copy_tracks=True`, the default): K2 reads the 8x8 quadrants of the occupied tiles in
-    place over PCIe (about a tenth of the track bytes at the benchmark configs); with
-    `zero_copy_tracks=False` the whole arrays are copied on the H2D stream.  Input slots and
+    from that engine's output buffer.  Tracks given as pinned host tensors need not be copied
+    (`zero_copy_tracks=True`): K2 reads the 8x8 quadrants of the occupied tiles in place over
+    PCIe (about a tenth of the track bytes at the benchmark configs, but at the PCIe request rate
+    rather than its bandwidth); with `zero_copy_tracks=False` the whole arrays are copied on the
+    H2D stream (DMA at full bandwidth, hidden when the compute takes longer).  The default
+    `"auto"` picks per step: it keeps the period between finished steps (CUDA events) and copies
+    the whole arrays whenever that copy -- estimated at `H2D_GBS` -- fits under the period,
+    reading in place otherwise.  Both modes give bit-identical results.  Input slots and
     output buffers are reused in turn, ordered with CUDA events.  `step` returns the event after
     which the previous step's results are in its host buffer (None for the first call);
     `flush()` runs the last pending step; `wait_all(stream)` orders `stream` after every result
@@ -227,9 +231,15 @@ class StreamingEngine:
 
     N_SLOTS = 4  # input slots: the copy of step k+1 never waits for steps k-1 / k-2
     N_ENGINES = 2  # frames in flight
+    H2D_GBS = 50.0  # pinned host -> device DMA rate assumed by the "auto" mode (GB/s)
 
-    def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks: bool = True):
+    def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
         torch = _torch()
+        self._compute_ms = None  # EMA of the step period ("auto" mode)
+        self._last_zero_copy = True
+        self.steps_zero_copy = 0  # steps whose tracks were read in place / copied whole
+        self.steps_full_copy = 0
+        self._timing = []  # (start, end) events of computed steps not yet read
         self.engines = [engine if engine is not None else FrameEngine()] + \
             [FrameEngine() for _ in range(self.N_ENGINES - 1)]
         self.zero_copy_tracks = zero_copy_tracks
@@ -280,14 +290,17 @@ class StreamingEngine:
         cs.wait_event(ready)
         if self._out_free[e] is not None:
             cs.wait_event(self._out_free[e])
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(cs)
         eng.bin(g_d, cameras, config, stream=cs)
         out = eng.compensate(t_d, v_d, self._outs[e], stream=cs)
         self._outs[e] = out
         with torch.cuda.stream(cs):
             res = torch.cat([out.delta_mean, out.rotation, out.scale,
                              out.status.to(torch.float64)[:, None]], 1)
-            computed = torch.cuda.Event()
+            computed = torch.cuda.Event(enable_timing=True)
             computed.record(cs)
+        self._timing.append((t0, computed))
         self._free[i] = computed
         ds = self.d2h_stream
         ds.wait_event(computed)
@@ -305,7 +318,12 @@ class StreamingEngine:
         torch = _torch()
         i = self._k % self.N_SLOTS
         self._k += 1
-        zero_copy = self.zero_copy_tracks and _pinned_pair(t_host, v_host)
+        zero_copy = self._choose_zero_copy(g_host, t_host, v_host) and \
+            _pinned_pair(t_host, v_host)
+        if zero_copy:
+            self.steps_zero_copy += 1
+        else:
+            self.steps_full_copy += 1
         g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host, not zero_copy)
         with torch.cuda.stream(self.copy_stream):
             if self._free[i] is not None:
@@ -321,10 +339,33 @@ class StreamingEngine:
         prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config)
         return self._compute(prev) if prev is not None else None
 
+    def _choose_zero_copy(self, g_host, t_host, v_host):
+        if self.zero_copy_tracks != "auto":
+            return bool(self.zero_copy_tracks)
+        # fold in the step period (interval between consecutive finished steps; never blocks):
+        # copying the whole arrays pays off when that copy fits under the period
+        # (over two steps: consecutive steps finish on alternating compute streams)
+        while len(self._timing) >= 3 and self._timing[2][1].query():
+            prev, cur = self._timing.pop(0), self._timing[1]
+            ms = 0.5 * prev[1].elapsed_time(cur[1])
+            self._compute_ms = ms if self._compute_ms is None else 0.7 * self._compute_ms + 0.3 * ms
+        if self._compute_ms is None:
+            return True
+        copy_ms = (g_host.numel() * g_host.element_size() + t_host.numel() *
+                   t_host.element_size() + v_host.numel()) / (self.H2D_GBS * 1e6)
+        # hysteresis: leave the current mode only on a clear margin
+        if self._last_zero_copy:
+            self._last_zero_copy = not copy_ms < 0.85 * self._compute_ms
+        else:
+            self._last_zero_copy = copy_ms > 0.95 * self._compute_ms
+        return self._last_zero_copy
+
     def flush(self):
         """Compute the last pending step; returns its results-ready event (or None)."""
         prev, self._pending = self._pending, None
-        return self._compute(prev) if prev is not None else None
+        done = self._compute(prev) if prev is not None else None
+        self._timing.clear()  # the next period would span the caller's idle time
+        return done
 
     def wait_all(self, stream):
         """Make `stream` wait for every result copy issued so far."""

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 from tests import golden_data as gd  # noqa: E402
 
 
-@pytest.mark.parametrize("zero_copy", [True, False])
+@pytest.mark.parametrize("zero_copy", [True, False, "auto"])
 def test_streaming_matches_direct(zero_copy):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
