@@ -409,11 +409,11 @@ void k2_stats_report(ts_plan *p, cudaStream_t s) {
   static const bool on = getenv("TS_K2_STATS") != nullptr;
   if (!on || !p->k2_stats.p) return;
   unsigned long long h[16];
-  cudaMemcpyAsync(h, p->k2_stats.p, 9 * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(h, p->k2_stats.p, 10 * 8, cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   fprintf(stderr, "K2 stats: units %llu chunks %llu instances %llu hits %llu skips %llu "
-          "eval_gauss %llu eval_pix %llu contrib %llu flushes %llu\n", h[0], h[1], h[2], h[3],
-          h[4], h[5], h[6], h[7], h[8]);
+          "eval_gauss %llu eval_pix %llu contrib %llu flushes %llu eval_empty %llu\n", h[0], h[1],
+          h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
 }
 
 ts_motions internal_motions(ts_plan *p) {

@@ -78,7 +78,7 @@ struct K2Params {
 #endif
 
 enum { K2S_UNITS, K2S_CHUNKS, K2S_INSTANCES, K2S_HITS, K2S_SKIPS, K2S_EVAL_GAUSS, K2S_EVAL_PIX,
-       K2S_CONTRIB, K2S_FLUSHES, K2S_N };
+       K2S_CONTRIB, K2S_FLUSHES, K2S_EVAL_EMPTY, K2S_N };
 
 template <typename TrackT>
 struct K2Warp {
@@ -335,7 +335,11 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
             const bool k0 = c0 && valid0, k1 = c1 && valid1;
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
             const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
-            if (K2_STATS_ON) st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
+            if (K2_STATS_ON) {
+              st[K2S_CONTRIB] += __popc(cm0) + __popc(cm1);
+              // evaluated but no pixel composited (bbox corner only: outside the ellipse)
+              if (!__any_sync(0xffffffffu, c0 || c1)) st[K2S_EVAL_EMPTY]++;
+            }
             if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
               if (k0) S.w[kpend][lane] = w0;
               if (k1) S.w[kpend][lane + 32] = w1;
