@@ -255,12 +255,13 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     # two frames in flight: steps alternate between two engines (binning plans) on two streams,
     # so one frame's binning fills the SMs that the other's latency-bound K3/K4 leave idle
-    engs = [eng, FrameEngine()]
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    outs = [None, None]
+    n_fly = int(os.environ.get("TS_FRAMES_IN_FLIGHT", "2"))
+    engs = [eng] + [FrameEngine() for _ in range(n_fly - 1)]
+    streams = [torch.cuda.Stream() for _ in range(n_fly)]
+    outs = [None] * n_fly
 
     def step(k):
-        i = k & 1
+        i = k % n_fly
         engs[i].bin(g_dev, cams, stream=streams[i])
         outs[i] = engs[i].compensate(tgt, val, outs[i], stream=streams[i])
         return i
@@ -320,7 +321,8 @@ def run_ours(args):
     eng.plan.timing(False)
     # free the second engine before the e2e runs (its partial-moment workspace is 128 B per bbox
     # quadrant: 27 GB at cfg5)
-    engs[1].plan.close()
+    for e_ in engs[1:]:
+        e_.plan.close()
     del engs, outs, streams
     torch.cuda.empty_cache()
     if world > 1:
@@ -420,7 +422,7 @@ def run_ours(args):
                        "height": h, "target_frame_per_rank": "gap*(rank+1)",
                        "frames_per_s": world / (ms / 1e3),
                        "parallelism": f"frame-sharded x{world}",
-                       "frames_in_flight": 2,
+                       "frames_in_flight": n_fly,
                        "l2": f"inputs larger than the 126 MB L2 (tracks {9 * nv * w * h / 1e6:.0f} MB, "
                              f"raster records {64 * n * nv / 1e6:.0f} MB per step); no flush"},
             "e2e": {"value": n * nv * world / (ms_e2e / 1e3), "unit": "Gaussian-views/s",
