@@ -1,0 +1,73 @@
+"""StreamingEngine's "auto" track policy (engine.py): copy the whole track arrays when that copy
+fits under the measured step period, read the occupied tiles in place otherwise, with hysteresis.
+Host logic only (fake CUDA events), so it runs on the CPU suite."""
+
+import pytest
+
+pytest.importorskip("torch")
+
+from paper_2604_02586_b200.engine import StreamingEngine  # noqa: E402
+
+
+class _Ev:
+    def __init__(self, t):
+        self.t = t
+
+    def query(self):
+        return True
+
+    def elapsed_time(self, other):
+        return other.t - self.t
+
+
+class _Arr:
+    def __init__(self, nbytes):
+        self.n = nbytes
+
+    def numel(self):
+        return self.n
+
+    def element_size(self):
+        return 1
+
+
+def _engine(period_ms, steps=8):
+    se = StreamingEngine.__new__(StreamingEngine)  # no CUDA streams needed for the policy
+    se.zero_copy_tracks = "auto"
+    se._compute_ms = None
+    se._last_zero_copy = True
+    se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms)) for k in range(steps)]
+    return se
+
+
+def _choose(se, mbytes):
+    # copy estimate = bytes / H2D_GBS
+    return se._choose_zero_copy(_Arr(0), _Arr(int(mbytes * 1e6)), _Arr(0))
+
+
+def test_auto_reads_in_place_when_the_copy_does_not_fit():
+    se = _engine(period_ms=4.4)
+    assert _choose(se, 273.0) is True          # 273 MB at 50 GB/s = 5.5 ms > 4.4 ms
+    assert se._compute_ms == pytest.approx(4.4)
+
+
+def test_auto_copies_when_the_copy_hides_under_the_compute():
+    se = _engine(period_ms=14.9)
+    assert _choose(se, 562.0) is False         # 11.2 ms < 0.85 * 14.9 ms
+
+
+def test_auto_hysteresis():
+    se = _engine(period_ms=5.0)
+    # in place: 4.4 ms copy is not below 0.85 * 5.0 = 4.25 ms -> stay in place
+    assert _choose(se, 220.0) is True
+    se._last_zero_copy = False
+    # copying: 4.4 ms is not above 0.95 * 5.0 = 4.75 ms -> keep copying
+    assert _choose(se, 220.0) is False
+
+
+def test_fixed_modes_ignore_the_period():
+    se = _engine(period_ms=1.0)
+    se.zero_copy_tracks = True
+    assert _choose(se, 1.0) is True
+    se.zero_copy_tracks = False
+    assert _choose(se, 1e6) is False
