@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
       __syncwarp();
       if (i < end) {
         const uint32_t gv = P.inst_gv[i];
+        // the partial-slot base is loaded beside the record (not after the hit test), so the
+        // chunk's dependent chain is inst_gv -> {record, slot base}
+        const uint32_t ibase = MODE == K2_ACCUMULATE ? __ldg(P.inst_base + gv) : 0u;
         const RasterRec r = P.rec[gv];
         const uint64_t rect = quad_rect(r, qx0, qy0);
         hit = (rect & ~done64) != 0ull;
@@ -298,8 +301,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
           if (MODE == K2_ACCUMULATE) {
             // one slot per 8x8 quadrant of the gv's bbox, row-major from its top-left quadrant
             const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
-            S.slot[lane] = P.inst_base[gv] + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
-                                                        ((qx0 >> 3) - bx0));
+            S.slot[lane] = ibase + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
+                                              ((qx0 >> 3) - bx0));
             S.anc[lane] = make_int2(anchor_x(r), anchor_y(r));
           } else {
             S.slot[lane] = gv;
