@@ -235,8 +235,10 @@ class StreamingEngine:
 
     def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
         torch = _torch()
-        self._compute_ms = None  # EMA of the step period ("auto" mode)
+        self._compute_ms = None  # median of the last step periods ("auto" mode)
+        self._periods = []
         self._last_zero_copy = True
+        self._burst = 0
         self.steps_zero_copy = 0  # steps whose tracks were read in place / copied whole
         self.steps_full_copy = 0
         self._timing = []  # (start, end) events of computed steps not yet read
@@ -300,7 +302,7 @@ class StreamingEngine:
                              out.status.to(torch.float64)[:, None]], 1)
             computed = torch.cuda.Event(enable_timing=True)
             computed.record(cs)
-        self._timing.append((t0, computed))
+        self._timing.append((t0, computed, self._burst))
         self._free[i] = computed
         ds = self.d2h_stream
         ds.wait_event(computed)
@@ -324,7 +326,9 @@ class StreamingEngine:
             self.steps_zero_copy += 1
         else:
             self.steps_full_copy += 1
-        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host, not zero_copy)
+        # "auto" keeps device track buffers in every slot, so a mode switch never allocates
+        g_d, t_d, v_d = self._slot(i, g_host, t_host, v_host,
+                                   not zero_copy or self.zero_copy_tracks == "auto")
         with torch.cuda.stream(self.copy_stream):
             if self._free[i] is not None:
                 self.copy_stream.wait_event(self._free[i])
@@ -347,8 +351,10 @@ class StreamingEngine:
         # (over two steps: consecutive steps finish on alternating compute streams)
         while len(self._timing) >= 3 and self._timing[2][1].query():
             prev, cur = self._timing.pop(0), self._timing[1]
-            ms = 0.5 * prev[1].elapsed_time(cur[1])
-            self._compute_ms = ms if self._compute_ms is None else 0.7 * self._compute_ms + 0.3 * ms
+            if prev[2] != cur[2]:  # the two steps straddle a flush (caller's idle time)
+                continue
+            self._periods = (self._periods + [0.5 * prev[1].elapsed_time(cur[1])])[-5:]
+            self._compute_ms = sorted(self._periods)[len(self._periods) // 2]  # robust median
         if self._compute_ms is None:
             return True
         copy_ms = (g_host.numel() * g_host.element_size() + t_host.numel() *
@@ -364,7 +370,7 @@ class StreamingEngine:
         """Compute the last pending step; returns its results-ready event (or None)."""
         prev, self._pending = self._pending, None
         done = self._compute(prev) if prev is not None else None
-        self._timing.clear()  # the next period would span the caller's idle time
+        self._burst += 1  # a period across this point would span the caller's idle time
         return done
 
     def wait_all(self, stream):

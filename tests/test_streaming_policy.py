@@ -35,8 +35,9 @@ def _engine(period_ms, steps=8):
     se = StreamingEngine.__new__(StreamingEngine)  # no CUDA streams needed for the policy
     se.zero_copy_tracks = "auto"
     se._compute_ms = None
+    se._periods = []
     se._last_zero_copy = True
-    se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms)) for k in range(steps)]
+    se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms), 0) for k in range(steps)]
     return se
 
 
@@ -71,3 +72,19 @@ def test_fixed_modes_ignore_the_period():
     assert _choose(se, 1.0) is True
     se.zero_copy_tracks = False
     assert _choose(se, 1e6) is False
+
+
+def test_periods_across_a_flush_are_ignored():
+    se = _engine(period_ms=4.0, steps=4)
+    # a burst boundary (flush) followed by a long idle gap: not a period
+    se._timing += [(_Ev(1000.0 + 4.0 * k), _Ev(1000.0 + 4.0 * k), 1) for k in range(4)]
+    _choose(se, 100.0)
+    assert se._compute_ms == pytest.approx(4.0)
+
+
+def test_period_estimate_is_robust_to_a_slow_first_step():
+    se = _engine(period_ms=4.0, steps=2)
+    se._timing = [(_Ev(0.0), _Ev(0.0), 0), (_Ev(30.0), _Ev(30.0), 0)] + \
+        [(_Ev(30.0 + 4.0 * k), _Ev(30.0 + 4.0 * k), 0) for k in range(1, 8)]
+    _choose(se, 100.0)
+    assert se._compute_ms == pytest.approx(4.0)
