@@ -276,12 +276,11 @@ def run_ours(args):
         gather_buf = [torch.empty((n, 11), dtype=torch.float64, device=dev) for _ in range(world)]
 
     def updated_rows(o):
-        rows = g_dev.clone()
-        keep = o.status != 0
-        rows[keep, 0:3] += o.delta_mean[keep]
-        rows[keep, 3:7] = o.rotation[keep]
-        rows[keep, 7:10] = o.scale[keep]
-        return rows
+        # torch.where, not boolean indexing: a masked index is a device->host sync (nonzero)
+        # that would stop the host from enqueueing the next frame while this one runs
+        keep = (o.status != 0)[:, None]
+        upd = torch.cat([g_dev[:, 0:3] + o.delta_mean, o.rotation, o.scale, g_dev[:, 10:]], 1)
+        return torch.where(keep, upd, g_dev)
 
     if world > 1:
         dist.barrier()
