@@ -22,8 +22,8 @@ cpu_baseline: the CPU oracle port (oracle/: C raster/accumulate, numpy/LAPACK so
      bounded sample, in a process pool over all host cores.
 --impl reference: the same CPU port as the reference arm, timed per step on a bounded sample.
 Multi-GPU (torchrun): weak scaling, one target frame per rank (short-clip frame sharding,
-pipeline.py:64-65): Gaussians broadcast from rank 0 once per clip over NCCL, updated Gaussians
-gathered to rank 0 over NCCL inside each step.
+pipeline.py:64-65): Gaussians broadcast from rank 0 once per clip over NCCL, each frame's updates
+gathered to rank 0 over NCCL inside each step (on a stream of their own).
 """
 
 from __future__ import annotations
@@ -260,27 +260,33 @@ def run_ours(args):
     streams = [torch.cuda.Stream() for _ in range(n_fly)]
     outs = [None] * n_fly
 
+    def update_tensors(o):
+        return (o.delta_mean, o.rotation, o.scale, o.status)
+
     def step(k):
         i = k % n_fly
+        if gather_bufs is not None and gather_ev[i] is not None:
+            streams[i].wait_event(gather_ev[i])  # outs[i] was last read by a gather
         engs[i].bin(g_dev, cams, stream=streams[i])
         outs[i] = engs[i].compensate(tgt, val, outs[i], stream=streams[i])
         return i
 
     for s_ in streams:
         s_.wait_stream(stream)
+    gather_bufs = None
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
-    gather_buf = None
     if world > 1:
-        gather_buf = [torch.empty((n, 11), dtype=torch.float64, device=dev) for _ in range(world)]
-
-    def updated_rows(o):
-        # torch.where, not boolean indexing: a masked index is a device->host sync (nonzero)
-        # that would stop the host from enqueueing the next frame while this one runs
-        keep = (o.status != 0)[:, None]
-        upd = torch.cat([g_dev[:, 0:3] + o.delta_mean, o.rotation, o.scale, g_dev[:, 10:]], 1)
-        return torch.where(keep, upd, g_dev)
+        # the updates of every rank's frame (delta mean, rotation, scale, status: 81 B per Gaussian)
+        # are gathered to rank 0, which holds the frame-1 Gaussians they apply to.  Gathered
+        # straight from the frame's output tensors on a stream of their own: no kernel is added to
+        # the frames' streams (row-forming torch kernels there queued behind the other frame's
+        # persistent K2 and cost ~1 ms per step), and a slot's outputs are rewritten only after
+        # their gather has read them
+        gather_bufs = [[torch.empty_like(t) for _ in range(world)] for t in update_tensors(outs[0])]
+        gather_stream = torch.cuda.Stream()
+        gather_ev = [None] * n_fly
 
     if world > 1:
         dist.barrier()
@@ -297,12 +303,17 @@ def run_ours(args):
             torch.cuda.nvtx.range_push("step")
             i = step(k)
             if world > 1:
-                stream.wait_stream(streams[i])
-                dist.gather(updated_rows(outs[i]), gather_buf if rank == 0 else None, dst=0)
-                streams[i].wait_stream(stream)  # step k+2 rewrites outs[i] after this read
+                gather_stream.wait_stream(streams[i])
+                with torch.cuda.stream(gather_stream):
+                    for t, buf in zip(update_tensors(outs[i]), gather_bufs):
+                        dist.gather(t, buf if rank == 0 else None, dst=0)
+                gather_ev[i] = torch.cuda.Event()
+                gather_ev[i].record(gather_stream)
             torch.cuda.nvtx.range_pop()
         for s_ in streams:
             stream.wait_stream(s_)
+        if world > 1:
+            stream.wait_stream(gather_stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
