@@ -72,12 +72,11 @@ def gather_frames(local, n_rows, target_frames, group=None, dst=0):
 
 def apply_rows(rows, delta, rotation, scale, status):
     """Updated Gaussian rows (apply_updates semantics, regularize.py:179-188) as tensor ops."""
-    out = rows.clone()
-    keep = status != 0
-    out[keep, 0:3] += delta[keep]
-    out[keep, 3:7] = rotation[keep]
-    out[keep, 7:10] = scale[keep]
-    return out
+    import torch
+    # torch.where instead of boolean indexing: no device->host sync (a masked index is a nonzero)
+    keep = (status != 0)[:, None]
+    upd = torch.cat([rows[:, 0:3] + delta, rotation, scale, rows[:, 10:]], 1)
+    return torch.where(keep, upd, rows)
 
 
 def compensate_clip_sharded(first_rows, cameras, tracks_by_frame, target_frames, config=None,
