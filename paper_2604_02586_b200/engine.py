@@ -290,24 +290,25 @@ class StreamingEngine:
         self._c += 1
         eng, cs = self.engines[e], self.comp_streams[e]
         cs.wait_event(ready)
-        if self._out_free[e] is not None:
-            cs.wait_event(self._out_free[e])
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(cs)
         eng.bin(g_d, cameras, config, stream=cs)
+        # the binning does not touch the outputs: only K2-K4 wait for their previous D2H
+        if self._out_free[e] is not None:
+            cs.wait_event(self._out_free[e])
         out = eng.compensate(t_d, v_d, self._outs[e], stream=cs)
         self._outs[e] = out
-        with torch.cuda.stream(cs):
-            res = torch.cat([out.delta_mean, out.rotation, out.scale,
-                             out.status.to(torch.float64)[:, None]], 1)
-            computed = torch.cuda.Event(enable_timing=True)
-            computed.record(cs)
+        computed = torch.cuda.Event(enable_timing=True)
+        computed.record(cs)
         self._timing.append((t0, computed, self._burst))
         self._free[i] = computed
         ds = self.d2h_stream
         ds.wait_event(computed)
         with torch.cuda.stream(ds):
-            res.record_stream(ds)
+            # rows packed on the D2H stream, not the compute stream: a kernel queued there after K4
+            # waits for the other frame's persistent K2 and holds back the next frame's binning
+            res = torch.cat([out.delta_mean, out.rotation, out.scale,
+                             out.status.to(torch.float64)[:, None]], 1)
             res_host.copy_(res, non_blocking=True)
             done = torch.cuda.Event()
             done.record(ds)
