@@ -255,8 +255,14 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     # two frames in flight: steps alternate between two engines (binning plans) on two streams,
     # so one frame's binning fills the SMs that the other's latency-bound K3/K4 leave idle
-    n_fly = int(os.environ.get("TS_FRAMES_IN_FLIGHT", "2"))
+    n_fly = int(os.environ.get("TS_FRAMES_IN_FLIGHT", "3"))
     engs = [eng] + [FrameEngine() for _ in range(n_fly - 1)]
+    # with frames in flight the persistent K2 grid is capped so the other frames' kernels share
+    # the SMs (cfg2, 3 in flight: 3 CTAs/SM 3.53 ms/step vs full grid 3.65); the per-stage times
+    # below run one frame alone with the full grid
+    k2_cap = int(os.environ.get("TS_K2_CTAS_PER_SM", "3")) if n_fly > 1 else 0
+    for e_ in engs:
+        e_.plan.set_k2_ctas_per_sm(k2_cap)
     streams = [torch.cuda.Stream() for _ in range(n_fly)]
     outs = [None] * n_fly
 
@@ -322,6 +328,7 @@ def run_ours(args):
     out = outs[0]
     # per-stage CUDA-event times (and K2's kernel time for the roofline) from separate
     # sequential steps on one stream, so the stages do not overlap another frame's work
+    eng.plan.set_k2_ctas_per_sm(0)
     eng.plan.timing(True)
     for _ in range(min(args.steps, 20)):
         eng.bin(g_dev, cams)
@@ -432,7 +439,7 @@ def run_ours(args):
                        "height": h, "target_frame_per_rank": "gap*(rank+1)",
                        "frames_per_s": world / (ms / 1e3),
                        "parallelism": f"frame-sharded x{world}",
-                       "frames_in_flight": n_fly,
+                       "frames_in_flight": n_fly, "k2_ctas_per_sm_in_flight": k2_cap,
                        "l2": f"inputs larger than the 126 MB L2 (tracks {9 * nv * w * h / 1e6:.0f} MB, "
                              f"raster records {64 * n * nv / 1e6:.0f} MB per step); no flush"},
             "e2e": {"value": n * nv * world / (ms_e2e / 1e3), "unit": "Gaussian-views/s",

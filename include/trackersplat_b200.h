@@ -96,6 +96,12 @@ int64_t ts_plan_workspace_bytes(const ts_plan *plan);
 #define TS_N_STAGES 6
 int ts_plan_timing(ts_plan *plan, int enable);
 int ts_plan_timing_read(ts_plan *plan, double *totals_ms, int32_t *counts, int32_t n_stages);
+/* Residency of the persistent K2 grid: at most ctas_per_sm CTAs per SM (0 = as many as fit, the
+ * default).  A plan whose frames run two or three in flight on separate streams does better with
+ * fewer (3 at cfg2: the other frame's binning, solve and fuse kernels share the SMs K2 leaves
+ * free); a frame run alone is fastest with the full grid.  No reference counterpart: a
+ * scheduling knob of this build (the reference's raster loop, splat.py:147-195, is serial). */
+int ts_plan_set_k2_ctas_per_sm(ts_plan *plan, int32_t ctas_per_sm);
 
 /* _project_all, splat.py:80-110.  mean2 (N,2), depth (N), cov2 (N,3: xx,xy,yy), in_front (N). */
 int ts_project(const double *gaussians, int64_t n, const ts_camera *camera, double *mean2,

@@ -91,6 +91,7 @@ _SIGS = {
     "ts_plan_workspace_bytes": ([_vp], ctypes.c_int64),
     "ts_plan_timing": ([_vp, ctypes.c_int], ctypes.c_int),
     "ts_plan_timing_read": ([_vp, _vp, _vp, ctypes.c_int32], ctypes.c_int),
+    "ts_plan_set_k2_ctas_per_sm": ([_vp, ctypes.c_int32], ctypes.c_int),
     "ts_project": ([_vp, ctypes.c_int64, ctypes.POINTER(Camera), _vp, _vp, _vp, _vp, _vp],
                    ctypes.c_int),
     "ts_frame_bin": ([_vp, _vp, ctypes.c_int64, ctypes.POINTER(Camera), ctypes.c_int32,
@@ -273,6 +274,11 @@ class Plan:
 
     def timing(self, enable=True):
         check(self._lib.ts_plan_timing(self.handle, int(bool(enable))), "ts_plan_timing")
+
+    def set_k2_ctas_per_sm(self, ctas_per_sm):
+        """Cap the persistent K2 grid at `ctas_per_sm` CTAs per SM (0: full residency)."""
+        check(self._lib.ts_plan_set_k2_ctas_per_sm(self.handle, int(ctas_per_sm)),
+              "ts_plan_set_k2_ctas_per_sm")
 
     def timing_read(self):
         tot = (ctypes.c_double * N_STAGES)()

@@ -74,6 +74,7 @@ struct ts_plan {
   std::vector<ts_camera> host_cams;
   ts_config cfg{};
   bool timing = false;
+  int k2_ctas_per_sm = 0;  // ts_plan_set_k2_ctas_per_sm (0: full residency)
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks;
   size_t ev_next = 0;
@@ -477,6 +478,12 @@ int ts_plan_destroy(ts_plan *p) {
 int64_t ts_plan_workspace_bytes(const ts_plan *p) { return p ? sum_workspace(p) : 0; }
 
 // Stage timing (CUDA events on the plan's launch stream), used by bench.py for the roofline.
+int ts_plan_set_k2_ctas_per_sm(ts_plan *p, int32_t ctas_per_sm) {
+  if (!p || ctas_per_sm < 0) return TS_E_INVALID_ARGUMENT;
+  p->k2_ctas_per_sm = ctas_per_sm;
+  return TS_OK;
+}
+
 int ts_plan_timing(ts_plan *p, int enable) {
   if (!p) return TS_E_INVALID_ARGUMENT;
   p->timing = enable != 0;
@@ -564,7 +571,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                         track_target, track_valid, p->W, p->H, p->tiles_x, p->tpv, p->cfg,
                         ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, k2_stats(p, s),
-                        p->k2_sched.p, s));
+                        p->k2_sched.p, s, p->k2_ctas_per_sm));
   k2_stats_report(p, s);
   p->mark_end(ST_RASTER, e3, s);
 

@@ -27,7 +27,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      unsigned long long *stats, void *schedule_ws, cudaStream_t s);
+                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm = 0);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
 
 // K3: per-(view, Gaussian) affine fit from the tile partials of K2.

@@ -469,7 +469,7 @@ size_t k2_schedule_bytes(int n_tiles) {
 }
 
 template <int MODE, typename TrackT>
-static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
+static cudaError_t launch_mode(const K2Params &P, cudaStream_t s, int cap) {
   auto kern = k2_raster<MODE, TrackT>;
   const size_t smem = K2_ETAB_BYTES + sizeof(K2Warp<TrackT>) * K2_WARPS;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -479,6 +479,9 @@ static cudaError_t launch_mode(const K2Params &P, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_WARPS * 32, smem);
   if (e != cudaSuccess) return e;
+  // the plan's residency cap (ts_plan_set_k2_ctas_per_sm): leaves SM room for the other frames
+  // in flight
+  if (cap > 0 && cap < per_sm) per_sm = cap;
   kern<<<sms * (per_sm > 0 ? per_sm : 1), K2_WARPS * 32, smem, s>>>(P);
   return cudaGetLastError();
 }
@@ -491,7 +494,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      unsigned long long *stats, void *schedule_ws, cudaStream_t s) {
+                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -542,11 +545,11 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.dom_depth = dom_depth;
   P.stats = stats;
   if (mode == K2_ACCUMULATE) {
-    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s);
-    return launch_mode<K2_ACCUMULATE, double>(P, s);
+    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
+    return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
   }
-  if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s);
-  return launch_mode<K2_DOMINANT, float>(P, s);
+  if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s, ctas_per_sm);
+  return launch_mode<K2_DOMINANT, float>(P, s, ctas_per_sm);
 }
 
 }  // namespace ts

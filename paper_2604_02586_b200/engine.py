@@ -232,6 +232,11 @@ class StreamingEngine:
     N_SLOTS = 4  # input slots: the copy of step k+1 never waits for steps k-1 / k-2
     N_ENGINES = 2  # frames in flight
     H2D_GBS = 50.0  # pinned host -> device DMA rate assumed by the "auto" mode (GB/s)
+    # K2 residency of the engines (ts_plan_set_k2_ctas_per_sm): with two frames in flight the
+    # persistent K2 grid capped at 3 CTAs per SM leaves room for the other frame's kernels
+    # (cfg2 e2e 4.45 -> 4.15 ms; K2 alone is slower, 2.10 -> 3.06 ms, so a frame run alone keeps
+    # the full grid)
+    K2_CTAS_PER_SM = 3
 
     def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
         torch = _torch()
@@ -244,6 +249,8 @@ class StreamingEngine:
         self._timing = []  # (start, end) events of computed steps not yet read
         self.engines = [engine if engine is not None else FrameEngine()] + \
             [FrameEngine() for _ in range(self.N_ENGINES - 1)]
+        for e_ in self.engines:
+            e_.plan.set_k2_ctas_per_sm(self.K2_CTAS_PER_SM)
         self.zero_copy_tracks = zero_copy_tracks
         self.copy_stream = torch.cuda.Stream()
         self.comp_streams = [torch.cuda.Stream() for _ in range(self.N_ENGINES)]

@@ -121,3 +121,22 @@ def test_argument_errors(scene7):
     many = np.repeat(cams[:1], 65, axis=0)
     with pytest.raises(ValueError):
         FrameEngine().bin(g[:10], many)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3])
+def test_k2_residency_cap_is_bit_identical(scene7, cap):
+    """ts_plan_set_k2_ctas_per_sm changes only how many warps pull K2's work queue: every
+    (tile, quadrant) unit is still walked by one warp in list order, so outputs are bit-identical."""
+    from paper_2604_02586_b200.engine import FrameEngine
+    g, cams, target, valid = scene7
+    a = _run(g, cams, target, valid)
+    eng = FrameEngine()
+    eng.plan.set_k2_ctas_per_sm(cap)
+    eng.bin(g, cams)
+    b = eng.compensate(target, valid.astype(np.uint8))
+    torch.cuda.synchronize()
+    for k in ("status", "delta_mean", "rotation", "scale", "pixel_count", "weight_sum",
+              "motion_status", "static_pixel_count"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+    with pytest.raises(Exception):
+        eng.plan.set_k2_ctas_per_sm(-1)
