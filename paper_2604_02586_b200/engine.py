@@ -208,11 +208,11 @@ class FrameEngine:
 class StreamingEngine:
     """Pipelined end-to-end driver: pinned host inputs in, pinned host results out.
 
-    Streams: one H2D stream, two compute streams and one D2H stream.  `step(inputs_k)` enqueues
+    Streams: one H2D stream, N_ENGINES compute streams and one D2H stream.  `step(inputs_k)` enqueues
     the H2D copy of step k's inputs and then the compute of the PREVIOUS step (k-1), so the copy
     of step k is already queued when step k-1's binning briefly synchronises the host (the
     instance count).  Consecutive steps compute on alternating engines (binning plans) and
-    compute streams, so two frames are in flight: one frame's binning fills the SMs that the
+    compute streams, so N_ENGINES frames are in flight: one frame's binning fills the SMs that the
     other's latency-bound K3/K4 leave idle.  The D2H of a step's results runs on its own stream
     from that engine's output buffer.  Tracks given as pinned host tensors need not be copied
     (`zero_copy_tracks=True`): K2 reads the 8x8 quadrants of the occupied tiles in place over
@@ -229,10 +229,10 @@ class StreamingEngine:
     returned by the call that computes step k has completed.
     """
 
-    N_SLOTS = 4  # input slots: the copy of step k+1 never waits for steps k-1 / k-2
-    N_ENGINES = 2  # frames in flight
+    N_ENGINES = 3  # frames in flight (cfg2 e2e, in place: 2 -> 4.15 ms, 3 -> 3.92 ms per step)
+    N_SLOTS = N_ENGINES + 2  # input slots: the copy of step k+1 never waits for a frame in flight
     H2D_GBS = 50.0  # pinned host -> device DMA rate assumed by the "auto" mode (GB/s)
-    # K2 residency of the engines (ts_plan_set_k2_ctas_per_sm): with two frames in flight the
+    # K2 residency of the engines (ts_plan_set_k2_ctas_per_sm): with frames in flight the
     # persistent K2 grid capped at 3 CTAs per SM leaves room for the other frame's kernels
     # (cfg2 e2e 4.45 -> 4.15 ms; K2 alone is slower, 2.10 -> 3.06 ms, so a frame run alone keeps
     # the full grid)
