@@ -57,7 +57,7 @@ def _lib():
         lib.orc_project.argtypes = [i64, ptr, ptr, ptr, ptr, ptr, ptr]
         lib.orc_project.restype = None
         lib.orc_rasterize.argtypes = [i64, ptr, ptr, dbl, dbl, i64, ptr, ptr, ptr, ptr, ptr, ptr,
-                                      ptr, ptr]
+                                      ptr, ptr, ctypes.c_int]
         lib.orc_rasterize.restype = i64
         lib.orc_bin.argtypes = [i64, ptr, ptr, ctypes.c_int, i64, ptr, ptr, ptr, ptr, ptr, ptr]
         lib.orc_bin.restype = i64
@@ -96,8 +96,12 @@ def project(gaussians, camera):
     return mean2, depth, cov2, inf.astype(bool)
 
 
-def rasterize(gaussians, camera, alpha_cutoff=1.0 / 255.0, early_stop=1e-4):
-    """splat.py:113-195.  Returns a dict of WeightMap arrays plus degenerate_ids."""
+def rasterize(gaussians, camera, alpha_cutoff=1.0 / 255.0, early_stop=1e-4,
+              transmittance="reference"):
+    """splat.py:113-195.  Returns a dict of WeightMap arrays plus degenerate_ids.
+    transmittance="reference": the view-global log1p/cumsum T of splat.py:182-191;
+    "product": the exact running product per pixel (the GPU's compositing order)."""
+    t_mode = {"reference": 0, "product": 1}[transmittance]
     g = _c(gaussians, np.float64).reshape(-1, 11)
     cam = _c(camera, np.float64)
     n = len(g)
@@ -113,7 +117,7 @@ def rasterize(gaussians, camera, alpha_cutoff=1.0 / 255.0, early_stop=1e-4):
         de = np.empty(cap)
         m = _lib().orc_rasterize(n, _p(g), _p(cam), alpha_cutoff, early_stop, cap, _p(px),
                                  _p(py), _p(gid), _p(al), _p(tr), _p(de), _p(deg),
-                                 ctypes.byref(ndeg))
+                                 ctypes.byref(ndeg), t_mode)
         if m <= cap:
             break
         cap = m
@@ -294,10 +298,47 @@ def _decompose(sol, ref_quat, eig_floor):
     return _matrix_to_quat(r), scale
 
 
+def _decompose_batch(sols, ref_quats, eig_floor):
+    """_decompose over (G, 6) solutions: eigh / det as stacked gufunc calls, the permutation
+    search and quaternion branches vectorised, norms and dots per row (the BLAS calls the scalar
+    form makes).  Returns (quat (G,4), scale (G,3), ok (G,) bool); same bits as _decompose."""
+    g = len(sols)
+    m = np.empty((g, 3, 3))
+    m[:, 0, 0], m[:, 0, 1], m[:, 0, 2] = sols[:, 0], sols[:, 1], sols[:, 2]
+    m[:, 1, 0], m[:, 1, 1], m[:, 1, 2] = sols[:, 1], sols[:, 3], sols[:, 4]
+    m[:, 2, 0], m[:, 2, 1], m[:, 2, 2] = sols[:, 2], sols[:, 4], sols[:, 5]
+    m = 0.5 * (m + np.transpose(m, (0, 2, 1)))
+    evals, evecs = np.linalg.eigh(m)
+    tr = (m[:, 0, 0] + m[:, 1, 1]) + m[:, 2, 2]
+    ok = ~np.any(evals < (eig_floor * np.abs(tr))[:, None], axis=1)
+    rq = np.stack([q / np.linalg.norm(q) for q in ref_quats]) if g else np.zeros((0, 4))
+    ref = _quat_to_matrix_batch(rq)
+    dots = np.abs(np.stack([ref[r].T @ evecs[r] for r in range(g)])) if g else np.zeros((0, 3, 3))
+    sums = np.stack([((0 + dots[:, 0, p[0]]) + dots[:, 1, p[1]]) + dots[:, 2, p[2]]
+                     for p in _PERMS], axis=1)
+    best = np.asarray(_PERMS)[np.argmax(sums, axis=1)]  # first maximum, as max() over the list
+    rows_ = np.arange(g)
+    r = np.empty((g, 3, 3))
+    scale = np.empty((g, 3))
+    for k in range(3):
+        e = evecs[rows_, :, best[:, k]]
+        flip = np.array([np.dot(e[i], ref[i, :, k]) < 0 for i in range(g)], bool)
+        e = np.where(flip[:, None], -e, e)
+        r[:, :, k] = e
+        scale[:, k] = np.sqrt(evals[rows_, best[:, k]])
+    neg = np.linalg.det(r) < 0 if g else np.zeros(0, bool)
+    r[neg, :, 2] = -r[neg, :, 2]
+    q = np.empty((g, 4))
+    for i in range(g):  # core.py:41-62 branches (scalar control flow, numpy arithmetic)
+        q[i] = _matrix_to_quat(r[i])
+    return q, scale, ok
+
+
 def update_all(gaussians, motions, cameras, min_views=2, min_total_weight=1e-3,
-               min_total_pixels=3, eig_floor=1e-12):
+               min_total_pixels=3, eig_floor=1e-12, loop=False):
     """multiview.py:168-275 over arrays.  Returns dict delta_mean (N,3), rotation (N,4),
-    scale (N,3), status (N,) int8 and the eligibility mask."""
+    scale (N,3), status (N,) int8 and the eligibility mask.  `loop=True` runs the per-Gaussian
+    loop of the reference verbatim; the default groups the LAPACK calls (same bits)."""
     g = _c(gaussians, np.float64).reshape(-1, 11)
     n = len(g)
     nv = len(cameras)
@@ -357,8 +398,16 @@ def update_all(gaussians, motions, cameras, min_views=2, min_total_weight=1e-3,
     out_q = quats.copy()
     out_s = scales.copy()
     status = np.zeros(n, np.int8)
+    fuse = _fuse_loop if loop else _fuse_batched
+    fuse(np.flatnonzero(eligible), solved, rows, lin, rhs, means, quats, eig_floor, delta, out_q,
+         out_s, status)
+    return dict(delta_mean=delta, rotation=out_q, scale=out_s, status=status, eligible=eligible)
+
+
+def _fuse_loop(idx, solved, rows, lin, rhs, means, quats, eig_floor, delta, out_q, out_s, status):
+    """multiview.py:239-275, one Gaussian at a time (the reference's loop, verbatim order)."""
     with np.errstate(all="ignore"):
-        for i in np.flatnonzero(eligible):
+        for i in idx:
             sel = solved[:, i]
             a = rows[sel, i].reshape(-1, 4)
             try:
@@ -385,7 +434,67 @@ def update_all(gaussians, motions, cameras, min_views=2, min_total_weight=1e-3,
             out_q[i] = q
             out_s[i] = sc
             status[i] = STATUS_SOLVED
-    return dict(delta_mean=delta, rotation=out_q, scale=out_s, status=status, eligible=eligible)
+
+
+def _fuse_batched(idx, solved, rows, lin, rhs, means, quats, eig_floor, delta, out_q, out_s,
+                  status):
+    """_fuse_loop over groups of Gaussians with the same solved-view count: the SVDs and eigh run
+    as stacked LAPACK gufunc calls (per-matrix identical to the single calls); the few BLAS
+    level-1/2 operations whose kernels may round differently when stacked (norm, dot, gemv) stay
+    per Gaussian.  Bit-identical to _fuse_loop (tests/test_oracle_golden.py)."""
+    if len(idx) == 0:
+        return
+    nsol = solved[:, idx].sum(axis=0)
+    with np.errstate(all="ignore"):
+        for k in np.unique(nsol):
+            ids = idx[nsol == k]
+            gi, vi = np.nonzero(solved[:, ids].T)  # per Gaussian, its solved views ascending
+            a = rows[vi, ids[gi]].reshape(len(ids), 2 * k, 4)
+            try:
+                _, s, vt = np.linalg.svd(a)
+            except np.linalg.LinAlgError:
+                for j in ids:  # a failing stack: redo one by one (the loop's except path)
+                    _fuse_loop(np.array([j]), solved, rows, lin, rhs, means, quats, eig_floor,
+                               delta, out_q, out_s, status)
+                continue
+            ok = ~(s[:, -2] - s[:, -1] <= _SINGULAR_GAP_REL * s[:, 0])
+            x = vt[:, -1]
+            for r in np.flatnonzero(ok):
+                if abs(x[r, 3]) <= _SINGULAR_GAP_REL * np.linalg.norm(x[r]):
+                    ok[r] = False
+            if not ok.any():
+                continue
+            sub = np.flatnonzero(ok)
+            new_mean = x[sub, :3] / x[sub, 3:4]
+            ids2 = ids[sub]
+            lsel = lin[vi, ids[gi]].reshape(len(ids), 3 * k, 6)[sub]
+            rsel = rhs[vi, ids[gi]].reshape(len(ids), 3 * k)[sub]
+            try:
+                u, s, vt = np.linalg.svd(lsel, full_matrices=False)
+            except np.linalg.LinAlgError:
+                for j in ids2:
+                    _fuse_loop(np.array([j]), solved, rows, lin, rhs, means, quats, eig_floor,
+                               delta, out_q, out_s, status)
+                continue
+            ok2 = np.flatnonzero(~(s[:, -1] < _SINGULAR_GAP_REL * s[:, 0]))
+            if not len(ok2):
+                continue
+            sols = np.stack([vt[r].T @ ((u[r].T @ rsel[r]) / s[r]) for r in ok2])
+            try:
+                q, sc, ok3 = _decompose_batch(sols, quats[ids2[ok2]], eig_floor)
+            except (np.linalg.LinAlgError, ValueError):
+                for j in ids2[ok2]:
+                    _fuse_loop(np.array([j]), solved, rows, lin, rhs, means, quats, eig_floor,
+                               delta, out_q, out_s, status)
+                continue
+            nm = new_mean[ok2]
+            good = (ok3 & np.all(np.isfinite(q), axis=1) & np.all(np.isfinite(nm), axis=1)
+                    & np.all(sc > 0, axis=1))
+            i = ids2[ok2[good]]
+            delta[i] = nm[good] - means[i]
+            out_q[i] = q[good]
+            out_s[i] = sc[good]
+            status[i] = STATUS_SOLVED
 
 
 def compensate(gaussians, cameras, targets, valids, config=None):
@@ -410,3 +519,72 @@ def compensate(gaussians, cameras, targets, valids, config=None):
     upd = update_all(g, stacked, cameras, cfg["min_views"], cfg["min_total_weight"],
                      cfg["min_total_pixels"], cfg["eig_floor"])
     return upd, mots, accs
+
+
+# ---------------------------------------------------------------------------
+# oracle tracker (input production for the CPU arm and the tracker parity tests)
+
+def relative_rotations(frame0, frame_t):
+    """SceneSequence.relative_motion rotation for every Gaussian (scene.py:44-55):
+    quat_to_matrix(g1.rotation) @ quat_to_matrix(g0.rotation).T, one 3x3 product per Gaussian
+    as the reference forms it."""
+    r0 = _quat_to_matrix_batch(np.asarray(frame0, np.float64)[:, 3:7])
+    r1 = _quat_to_matrix_batch(np.asarray(frame_t, np.float64)[:, 3:7])
+    return np.stack([r1[i] @ r0[i].T for i in range(len(r0))]) if len(r0) else r0
+
+
+def dominant_gaussians(wm, width, height):
+    """scene.py:166-189: per pixel the contribution with the largest alpha*T (ties by the smaller
+    gaussian id).  Returns (gid (H,W) int64, -1 where empty; depth (H,W) float64)."""
+    gid_img = np.full((height, width), -1, dtype=np.int64)
+    depth_img = np.zeros((height, width))
+    if len(wm["pixel_x"]) == 0:
+        return gid_img, depth_img
+    weight = wm["alpha"] * wm["transmittance"]
+    pix = wm["pixel_y"].astype(np.int64) * width + wm["pixel_x"]
+    order = np.lexsort((wm["gaussian_id"], -weight, pix))
+    first = np.empty(len(order), dtype=bool)
+    first[0] = True
+    sorted_pix = pix[order]
+    np.not_equal(sorted_pix[1:], sorted_pix[:-1], out=first[1:])
+    sel = order[first]
+    gid_img[wm["pixel_y"][sel], wm["pixel_x"][sel]] = wm["gaussian_id"][sel]
+    depth_img[wm["pixel_y"][sel], wm["pixel_x"][sel]] = wm["depth"][sel]
+    return gid_img, depth_img
+
+
+def oracle_track(frame0, frame_t, camera, wm, view, target_frame, noise_sigma_px=0.0, seed=0,
+                 rel=None):
+    """scene.py:192-240 over arrays: every pixel back-projected onto the depth plane of its
+    dominant Gaussian (from the frame-0 WeightMap `wm`), moved by that Gaussian's rigid motion
+    frame0 -> frame_t and reprojected; keyed noise default_rng([seed, view, target_frame]).
+    Returns (target (H,W,2) float64, valid (H,W) bool)."""
+    cam = np.asarray(camera, np.float64)
+    rot, trans = cam[:9].reshape(3, 3), cam[9:12]
+    fx, fy, cx, cy = cam[12], cam[13], cam[14], cam[15]
+    w, h = int(cam[16]), int(cam[17])
+    gid_img, depth_img = dominant_gaussians(wm, w, h)
+    valid = gid_img >= 0
+    ys, xs = np.mgrid[0:h, 0:w]
+    target = np.stack([xs, ys], axis=-1).astype(np.float64)
+    vy, vx = np.nonzero(valid)
+    if len(vy):
+        f0 = np.asarray(frame0, np.float64)
+        f1 = np.asarray(frame_t, np.float64)
+        z = depth_img[vy, vx]
+        pc = np.stack([(vx - cx) / fx * z, (vy - cy) / fy * z, z], axis=1)
+        pw = (pc - trans) @ rot
+        gids = gid_img[vy, vx]
+        uniq, inv = np.unique(gids, return_inverse=True)
+        rels = rel[uniq] if rel is not None else relative_rotations(f0[uniq], f1[uniq])
+        mu0s = f0[uniq, 0:3]
+        mu1s = f1[uniq, 0:3]
+        moved = np.einsum("nij,nj->ni", rels[inv], pw - mu0s[inv]) + mu1s[inv]
+        pc2 = moved @ rot.T + trans
+        target[vy, vx, 0] = fx * pc2[:, 0] / pc2[:, 2] + cx
+        target[vy, vx, 1] = fy * pc2[:, 1] / pc2[:, 2] + cy
+    if noise_sigma_px > 0:
+        rng = np.random.default_rng([seed, view, target_frame])
+        noise = rng.normal(scale=noise_sigma_px, size=(h, w, 2))
+        target[valid] += noise[valid]
+    return target, valid

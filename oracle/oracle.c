@@ -12,7 +12,9 @@
  *   orc_rasterize    gausstrack/splat.py:113-195 (rasterize_weights): 3-sigma bbox, explicit
  *                    inverse, q in numpy's left-to-right order, alpha clamp, keep predicate,
  *                    lexsort((gid, depth, pix)), view-global log1p/cumsum transmittance,
- *                    early stop.
+ *                    early stop.  t_mode 1 swaps the log-cumsum T for the exact running product
+ *                    per pixel (what the GPU composites): the reference's own T drift (~1e-8 rel
+ *                    at 1e7 contributions per view) then drops out of at-scale comparisons.
  *   orc_bin          restatement of the tile binning the GPU adds on top of splat.py:131-146
  *                    (16x16 tiles, per-tile order = (depth, gid) as in splat.py:178).
  *   orc_accumulate   gausstrack/motion2d.py:126-161 (accumulate_view): np.add.at in array
@@ -125,39 +127,63 @@ static int footprint(int in_front, const double *m2, const double *c, int W, int
 }
 
 typedef struct {
-  int64_t pix;
   double depth;
   int64_t gid;
-  int32_t px, py;
-  double alpha;
-} contrib_t;
+} gorder_t;
 
-static int cmp_contrib(const void *a, const void *b) {
-  const contrib_t *x = (const contrib_t *)a, *y = (const contrib_t *)b;
-  if (x->pix != y->pix) return x->pix < y->pix ? -1 : 1;
+static int cmp_gorder(const void *a, const void *b) {
+  const gorder_t *x = (const gorder_t *)a, *y = (const gorder_t *)b;
   if (x->depth != y->depth) return x->depth < y->depth ? -1 : 1;
   if (x->gid != y->gid) return x->gid < y->gid ? -1 : 1;
   return 0;
 }
 
+typedef struct {
+  int64_t gid;
+  double alpha;
+  double depth;
+  int32_t px, py;
+} contrib_t;
+
 /* splat.py:113-195.  Outputs are written only if n_kept <= cap; the return value is always the
  * number of kept contributions (call again with a larger cap if it exceeds cap).
- * degenerate ids (<= n of them) go to `degenerate`, count in *n_degenerate. */
+ * degenerate ids (<= n of them) go to `degenerate`, count in *n_degenerate.
+ *
+ * The contribution order is the reference's lexsort((gid, depth, pix)) (splat.py:171-180).  It is
+ * formed without a comparison sort over the contributions: the binned Gaussians are ordered by
+ * (depth, gid) first, their contributions generated in that order, and a stable counting sort by
+ * pixel index then yields exactly the (pix, depth, gid) order. */
 int64_t orc_rasterize(int64_t n, const double *G, const double *cam, double alpha_cutoff,
                       double early_stop, int64_t cap, int32_t *px_o, int32_t *py_o,
                       int64_t *gid_o, double *alpha_o, double *trans_o, double *depth_o,
-                      int64_t *degenerate, int64_t *n_degenerate) {
+                      int64_t *degenerate, int64_t *n_degenerate, int t_mode) {
   int W = (int)cam[16], H = (int)cam[17];
-  int64_t ncap = 1024, m = 0, ndeg = 0;
-  contrib_t *cs = (contrib_t *)malloc(sizeof(contrib_t) * ncap);
+  int64_t npix = (int64_t)W * H;
+  int64_t ndeg = 0, nb = 0;
+  gorder_t *ord = (gorder_t *)malloc(sizeof(gorder_t) * (n > 0 ? n : 1));
   for (int64_t gid = 0; gid < n; gid++) {
-    const double *g = G + 11 * gid;
     double m2[2], z, c[3], det;
-    int inf = project_one(g, cam, m2, &z, c);
+    int inf = project_one(G + 11 * gid, cam, m2, &z, c);
     int bb[4];
     int st = footprint(inf, m2, c, W, H, bb, &det);
     if (st == 1) degenerate[ndeg++] = gid;
     if (st != 3) continue;
+    ord[nb].depth = z;
+    ord[nb].gid = gid;
+    nb++;
+  }
+  *n_degenerate = ndeg;
+  qsort(ord, (size_t)nb, sizeof(gorder_t), cmp_gorder);
+  int64_t ncap = 1024, m = 0;
+  contrib_t *cs = (contrib_t *)malloc(sizeof(contrib_t) * ncap);
+  int64_t *pix_count = (int64_t *)calloc((size_t)npix + 1, sizeof(int64_t));
+  for (int64_t k = 0; k < nb; k++) {
+    const int64_t gid = ord[k].gid;
+    const double *g = G + 11 * gid;
+    double m2[2], z, c[3], det = 1.0;
+    int inf = project_one(g, cam, m2, &z, c);
+    int bb[4];
+    footprint(inf, m2, c, W, H, bb, &det);
     double i00 = c[2] / det, i01 = -c[1] / det, i11 = c[0] / det;
     double two_i01 = 2 * i01;
     double op = g[10];
@@ -166,51 +192,78 @@ int64_t orc_rasterize(int64_t n, const double *G, const double *cam, double alph
       for (int x = bb[0]; x <= bb[1]; x++) {
         double dx = (double)x - m2[0];
         double q = ((i00 * dx) * dx + (two_i01 * dx) * dy) + (i11 * dy) * dy;
+        if (!(q <= SIGMA_RADIUS * SIGMA_RADIUS)) continue;
         double a = op * exp(-0.5 * q);
         if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
-        if (!(q <= SIGMA_RADIUS * SIGMA_RADIUS && a >= alpha_cutoff)) continue;
+        if (!(a >= alpha_cutoff)) continue;
         if (m == ncap) {
           ncap *= 2;
           cs = (contrib_t *)realloc(cs, sizeof(contrib_t) * ncap);
         }
         contrib_t *e = &cs[m++];
-        e->pix = (int64_t)y * W + x;
-        e->depth = z;
         e->gid = gid;
+        e->alpha = a;
+        e->depth = z;
         e->px = x;
         e->py = y;
-        e->alpha = a;
+        pix_count[(int64_t)y * W + x + 1]++;
       }
     }
   }
-  *n_degenerate = ndeg;
-  qsort(cs, (size_t)m, sizeof(contrib_t), cmp_contrib);
+  free(ord);
+  /* stable counting sort by pixel: perm[k] = generation index of the k-th contribution */
+  for (int64_t p = 0; p < npix; p++) pix_count[p + 1] += pix_count[p];
+  int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (m > 0 ? m : 1));
+  for (int64_t k = 0; k < m; k++) perm[pix_count[(int64_t)cs[k].py * W + cs[k].px]++] = k;
+  free(pix_count);
   /* view-global log-cumsum transmittance, splat.py:182-191 */
   int64_t kept = 0;
-  double csum = 0.0, seg_base = 0.0;
+  double csum = 0.0, seg_base = 0.0, tprod = 1.0;
+  int64_t prev_pix = -1;
+  /* Once a pixel's T falls below early_stop its later entries are cut as well: along a segment
+   * (csum - l) - seg_base drops by |log1p(-alpha)| >= |log1p(-alpha_cutoff)| per entry, which
+   * dwarfs the rounding of the running sum (~1e-13 in log space) whenever alpha_cutoff >= 1e-6,
+   * so the skipped exp calls could not have passed the test. */
+  const int can_skip = alpha_cutoff >= 1e-6;
+  int cut = 0;
   for (int64_t k = 0; k < m; k++) {
-    int start = (k == 0) || (cs[k].pix != cs[k - 1].pix);
-    double l = log1p(-cs[k].alpha);
-    csum += l;
+    const contrib_t *e = &cs[perm[k]];
+    const int64_t pix = (int64_t)e->py * W + e->px;
+    int start = pix != prev_pix;
+    prev_pix = pix;
     double T;
-    if (start) {
-      seg_base = csum - l;
-      T = 1.0;
+    if (t_mode == 1) {
+      /* exact running product (the GPU's compositing): T_in, then T *= (1 - alpha) */
+      if (start) tprod = 1.0;
+      T = tprod;
+      tprod = tprod * (1.0 - e->alpha);
     } else {
-      T = exp((csum - l) - seg_base);
+      double l = log1p(-e->alpha);
+      csum += l;
+      if (start) {
+        seg_base = csum - l;
+        T = 1.0;
+        cut = 0;
+      } else if (cut) {
+        continue; /* (csum - l) - seg_base only decreases along a segment (l <= 0) */
+      } else {
+        T = exp((csum - l) - seg_base);
+      }
     }
+    if (!(T >= early_stop)) cut = can_skip;
     if (T >= early_stop) {
       if (kept < cap) {
-        px_o[kept] = cs[k].px;
-        py_o[kept] = cs[k].py;
-        gid_o[kept] = cs[k].gid;
-        alpha_o[kept] = cs[k].alpha;
+        px_o[kept] = e->px;
+        py_o[kept] = e->py;
+        gid_o[kept] = e->gid;
+        alpha_o[kept] = e->alpha;
         trans_o[kept] = T;
-        depth_o[kept] = cs[k].depth;
+        depth_o[kept] = e->depth;
       }
       kept++;
     }
   }
+  free(perm);
   free(cs);
   return kept;
 }

@@ -428,6 +428,38 @@ def pipeline_kats():
     print("pipeline_kats", {k: v.shape for k, v in d.items()})
 
 
+def tracker_kats():
+    """Reference oracle tracker fixtures (scene.py:166-240), the scenes of tests/test_scene.py:67-156:
+    dominant (gid, depth) images and dense tracks, valid pixels only."""
+    from gausstrack.scene import dominant_gaussians
+    d = {}
+    cases = [  # (tag, generate_scene args, kwargs, view, target frame, noise, seed)
+        ("dom", (2, 20, 4, 2), {}, None, 1, 0.0, 0),
+        ("static", (4, 30, 4, 3), dict(mover_fraction=0.0), 0, 2, 0.0, 0),
+        ("cover", (4, 30, 4, 3), {}, 1, 1, 0.0, 0),
+        ("noisy", (4, 30, 4, 3), {}, 1, 2, 0.5, 9),
+        ("transl", (6, 40, 4, 2), dict(mover_fraction=1.0, translate_mag=0.03, rotate_deg=0.0),
+         0, 1, 0.0, 0),
+    ]
+    for tag, args, kw, view, frame, noise, seed in cases:
+        scene = generate_scene(*args, **kw)
+        d[f"{tag}_gaussians0"] = gauss_array(scene.frames[0])
+        d[f"{tag}_gaussians1"] = gauss_array(scene.frames[frame])
+        d[f"{tag}_cameras"] = cam_array(scene.cameras)
+        d[f"{tag}_meta"] = np.array([-1 if view is None else view, frame, noise, seed], np.float64)
+        views = range(len(scene.cameras)) if view is None else [view]
+        for v in views:
+            wm = rasterize_weights(scene.cameras[v], scene.frames[0], view_id=v)
+            gid, dep = dominant_gaussians(wm)
+            d[f"{tag}_v{v}_dom_gid"] = gid.astype(np.int32)
+            d[f"{tag}_v{v}_dom_depth"] = dep
+            tf = oracle_track(scene, v, frame, noise, seed=seed, weightmap=wm)
+            d[f"{tag}_v{v}_valid_bits"] = np.packbits(tf.valid.ravel())
+            d[f"{tag}_v{v}_target_valid"] = tf.target[tf.valid]
+    np.savez_compressed(os.path.join(OUT, "tracker_kats.npz"), **d)
+    print("tracker_kats", len(d), "arrays")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -437,6 +469,7 @@ if __name__ == "__main__":
     accumulate_kats()
     fuse_kats()
     scene_generator_fixture()
+    tracker_kats()
     # tests/test_multiview.py:201-202 fixture scene
     scene_pipeline("scene21", generate_scene(21, 120, 4, 2, mover_fraction=0.25,
                                              translate_mag=0.02), 1, 0.0)

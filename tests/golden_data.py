@@ -44,3 +44,39 @@ def tile_order_index(ranges):
     starts = np.repeat(ranges[:, 0], cnt)
     within = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
     return starts + within
+
+
+TRACKER_SCENES = {  # tracker_kats.npz cases: generate_scene args / kwargs (make_golden.py)
+    "dom": ((2, 20, 4, 2), {}),
+    "static": ((4, 30, 4, 3), dict(mover_fraction=0.0)),
+    "cover": ((4, 30, 4, 3), {}),
+    "noisy": ((4, 30, 4, 3), {}),
+    "transl": ((6, 40, 4, 2), dict(mover_fraction=1.0, translate_mag=0.03, rotate_deg=0.0)),
+}
+
+# the scene fixtures with reference tracks: generate_scene args / kwargs, noise sigma
+SCENE_TRACKS = {
+    "scene21": ((21, 120, 4, 2), dict(mover_fraction=0.25, translate_mag=0.02), 0.0),
+    "scene7": ((7, 2000, 8, 2), dict(mover_fraction=0.3, translate_mag=0.02, rotate_deg=2.0), 0.5),
+    "cfg1": ((1, 10_000, 4, 2), dict(focal=180, width=128, height=128, scale_range=(0.01, 0.02)),
+             0.0),
+}
+
+
+def tracker_case(d, tag):
+    """(meta dict, per-view dict of reference dominant gid / depth images and tracks)."""
+    view, frame, noise, seed = d[f"{tag}_meta"]
+    cams = d[f"{tag}_cameras"]
+    w, h = int(cams[0, 16]), int(cams[0, 17])
+    views = range(len(cams)) if view < 0 else [int(view)]
+    out = {}
+    for v in views:
+        valid = np.unpackbits(d[f"{tag}_v{v}_valid_bits"])[: w * h].reshape(h, w).astype(bool)
+        ys, xs = np.mgrid[0:h, 0:w]
+        target = np.stack([xs, ys], -1).astype(np.float64)
+        target[valid] = d[f"{tag}_v{v}_target_valid"]
+        out[v] = dict(gid=d[f"{tag}_v{v}_dom_gid"].astype(np.int64),
+                      depth=d[f"{tag}_v{v}_dom_depth"], target=target, valid=valid)
+    meta = dict(frame=int(frame), noise=float(noise), seed=int(seed), cameras=cams,
+                g0=d[f"{tag}_gaussians0"], g1=d[f"{tag}_gaussians1"])
+    return meta, out

@@ -1,16 +1,19 @@
-"""GPU parity at benchmark scale (BASELINE configs[1] and [2]) against the CPU oracle.
+"""GPU parity at benchmark scale (BASELINE configs[1]..[4]) against the CPU oracle.
 
 The inputs are generated on the box (restated generate_scene + the GPU oracle tracker, TRKF f32
-tracks); both sides consume the same arrays.  The oracle is run on a subset of views / a sample of
-Gaussians so the test stays within a minute:
-  * binning (status, bbox, per-tile (depth, gid) lists, tile ranges): bit-exact;
-  * pixel / static counts of the fused raster-accumulate: bit-exact;
-  * weight sums rel 1e-7 and moved means A mu + b within 5e-5 px: at this scale the reference's
-    view-global log-cumsum transmittance (splat.py:186-190) carries ~1e-8 relative error (SURVEY
-    §8(c): 6.9e-9 at cfg2) while K2 uses the exact running product, so the oracle is the less
-    accurate side; the contract bound for T is rel 1e-6;
-  * per-view statuses: flips <= 1e-4 of the Gaussians;
-  * K4 on the GPU's own motions vs the oracle update_all for a sample: SURVEY §8(c) tolerances.
+tracks); both sides consume the same arrays.  The oracle runs on sampled views and a sample of
+Gaussians so each config stays within a minute or two.
+
+Two oracle variants per sampled view (oracle.rasterize `transmittance=`):
+  * "product": the exact running product T per pixel -- what K2 composites.  Against it the
+    SURVEY §8(c) contract holds as written: contribution counts bit-exact, per-view statuses
+    flip <= 1e-4, moved means A mu + b within 1e-6 px, weight sums rel 1e-9 (summation order);
+  * "reference": the reference's view-global log1p/cumsum T (splat.py:182-191), whose own
+    rounding drifts by ~eps * |sum log1p(-alpha)| over a view (6.9e-9 at cfg2,
+    ~1e-7 at cfg5).  Against it: T-contract rel 1e-6 on the weight sums, count flips only at the
+    early-stop boundary (<= 1e-5 of the contributing gvs), observed maxima printed.
+Binning (status, per-tile (depth, gid) lists, tile ranges) is bit-exact.  K4 on the GPU's own
+motions vs the oracle update_all for a 2000-Gaussian sample: SURVEY §8(c) tolerances.
 """
 
 import numpy as np
@@ -29,6 +32,12 @@ CFGS = {
     "cfg3": dict(args=(0, 200_000, 27, 7), kw=dict(focal=520, width=640, height=360,
                                                    translate_mag=0.12, rotate_deg=3.0),
                  frame=6, views=(0, 13, 26)),
+    # configs[3]: the last target frame of the 9-frame clip (largest displacement)
+    "cfg4": dict(args=(0, 500_000, 20, 9), kw=dict(focal=1100, width=1352, height=1014),
+                 frame=8, views=(0, 10)),
+    # configs[4]: 3M Gaussians, 16 views 1920x1080
+    "cfg5": dict(args=(0, 3_000_000, 16, 2), kw=dict(focal=1400, width=1920, height=1080),
+                 frame=1, views=(0,)),
 }
 
 
@@ -45,12 +54,16 @@ def run(request):
     out = eng.compensate(tgt, val)
     torch.cuda.synchronize()
     cams = np.array([cm.as_row() for cm in scene.cameras])
-    return dict(name=request.param, scene=scene, eng=eng, tgt=tgt, val=val, out=out,
-                cams=cams, views=c["views"])
+    res = dict(name=request.param, g=scene.frames[0], eng=eng, tgt=tgt, val=val, out=out,
+               cams=cams, views=c["views"])
+    yield res
+    res.clear()
+    del eng, out, tgt, val
+    torch.cuda.empty_cache()
 
 
 def test_binning_bit_exact_at_scale(run):
-    g, cams, eng = run["scene"].frames[0], run["cams"], run["eng"]
+    g, cams, eng = run["g"], run["cams"], run["eng"]
     n = len(g)
     b = eng.binning()
     tpv = b["tiles_x"] * b["tiles_y"]
@@ -65,35 +78,55 @@ def test_binning_bit_exact_at_scale(run):
                                       ref["inst_gid"])
 
 
+def _moved(mu, a, b):
+    return np.einsum("nij,nj->ni", a, mu) + b
+
+
 def test_counts_and_motions_at_scale(run):
-    g, cams, out = run["scene"].frames[0], run["cams"], run["out"]
+    g, cams, out = run["g"], run["cams"], run["out"]
     n = len(g)
+    cnt_all = out.pixel_count.cpu().numpy()
+    scnt_all = out.static_pixel_count.cpu().numpy()
+    w_all = out.weight_sum.cpu().numpy()
+    st_all = out.motion_status.cpu().numpy()
+    a_all, b_all = out.motion_a.cpu().numpy(), out.motion_b.cpu().numpy()
     for v in run["views"]:
         tgt = run["tgt"][v].cpu().numpy().astype(np.float64)
         val = run["val"][v].cpu().numpy().astype(bool)
-        wm = oracle.rasterize(g, cams[v])
-        acc = oracle.accumulate(wm, tgt, val, n)
         sl = slice(v * n, (v + 1) * n)
-        np.testing.assert_array_equal(out.pixel_count.cpu().numpy()[sl], acc["pixel_count"])
-        np.testing.assert_array_equal(out.static_pixel_count.cpu().numpy()[sl],
-                                      acc["static_pixel_count"])
-        np.testing.assert_allclose(out.weight_sum.cpu().numpy()[sl], acc["weight_sum"],
-                                   rtol=1e-7, atol=1e-300)
-        sv = oracle.solve_view(acc)
-        st = out.motion_status.cpu().numpy()[sl]
-        flips = np.flatnonzero(st != sv["status"])
-        assert len(flips) <= max(2, 1e-4 * n), f"{run['name']} view {v}: {len(flips)} flips"
-        both = (st == 1) & (sv["status"] == 1)
         mu = oracle.project(g, cams[v])[0]
-        got = np.einsum("nij,nj->ni", out.motion_a.cpu().numpy()[sl], mu) + \
-            out.motion_b.cpu().numpy()[sl]
-        ref = np.einsum("nij,nj->ni", sv["a"], mu) + sv["b"]
-        err = np.abs(got - ref)[both].max()
-        assert err < 5e-5, f"{run['name']} view {v}: moved-mean error {err:.3g} px"
+        got_moved = _moved(mu, a_all[sl], b_all[sl])
+        report = {}
+        for mode in ("product", "reference"):
+            wm = oracle.rasterize(g, cams[v], transmittance=mode)
+            acc = oracle.accumulate(wm, tgt, val, n)
+            sv = oracle.solve_view(acc)
+            cnt_diff = np.flatnonzero((cnt_all[sl] != acc["pixel_count"])
+                                      | (scnt_all[sl] != acc["static_pixel_count"]))
+            has = acc["weight_sum"] > 0
+            wrel = np.abs(w_all[sl] - acc["weight_sum"])[has] / acc["weight_sum"][has]
+            flips = np.flatnonzero(st_all[sl] != sv["status"])
+            both = (st_all[sl] == 1) & (sv["status"] == 1)
+            merr = np.abs(got_moved - _moved(mu, sv["a"], sv["b"]))[both]
+            report[mode] = dict(count_diffs=len(cnt_diff), wsum_rel_max=float(wrel.max()),
+                                status_flips=len(flips),
+                                moved_mean_max_px=float(merr.max()) if merr.size else 0.0,
+                                solved=int(both.sum()))
+            if mode == "product":
+                assert len(cnt_diff) == 0, f"{run['name']} view {v}: counts differ {cnt_diff[:8]}"
+                assert wrel.max() <= 1e-9
+                assert len(flips) <= max(1, 1e-4 * n), f"{len(flips)} status flips"
+                assert merr.size == 0 or merr.max() <= 1e-6, f"moved mean {merr.max():.3g} px"
+            else:
+                assert len(cnt_diff) <= max(2, 1e-5 * has.sum())
+                ok = np.isin(np.arange(n)[has], cnt_diff, invert=True)
+                assert wrel[ok].max() <= 1e-6
+                assert len(flips) <= max(2, 1e-4 * n)
+        print(f"{run['name']} view {v}: {report}")
 
 
 def test_fuse_sample_at_scale(run):
-    g, cams, out = run["scene"].frames[0], run["cams"], run["out"]
+    g, cams, out = run["g"], run["cams"], run["out"]
     n, nv = len(g), len(cams)
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(n, size=2000, replace=False))
@@ -107,10 +140,13 @@ def test_fuse_sample_at_scale(run):
     flips = np.flatnonzero(st != ref["status"])
     assert len(flips) <= 2, flips
     both = (st == 1) & (ref["status"] == 1)
-    assert both.sum() > 100
+    assert both.sum() > (20 if run["name"] == "cfg5" else 100)
     d = out.delta_mean.cpu().numpy()[idx]
     mean_ref = g[idx, 0:3] + ref["delta_mean"]
     rel = np.linalg.norm((g[idx, 0:3] + d) - mean_ref, axis=1) / np.linalg.norm(mean_ref, axis=1)
     assert np.sum(rel[both] > 1e-4) <= 1
     s = out.scale.cpu().numpy()[idx]
-    assert np.sum((np.abs(s - ref["scale"]) / ref["scale"]).max(1)[both] > 1e-4) <= 1
+    srel = (np.abs(s - ref["scale"]) / ref["scale"]).max(1)
+    assert np.sum(srel[both] > 1e-4) <= 1
+    print(f"{run['name']} fuse sample: {int(both.sum())} solved, flips {len(flips)}, "
+          f"mean rel max {rel[both].max():.3g}, scale rel max {srel[both].max():.3g}")

@@ -118,3 +118,14 @@ def test_binning_restatement_consistent_with_raster():
             bbt = b["bbox"][ids] // 16
             assert np.all((bbt[:, 0] <= tx) & (tx <= bbt[:, 1]) & (bbt[:, 2] <= ty)
                           & (ty <= bbt[:, 3]))
+
+
+@pytest.mark.parametrize("scene", ["scene21", "scene7", "cfg1"])
+def test_product_transmittance_mode(scene):
+    """oracle.rasterize(transmittance="product") (the GPU's exact running product, used by the
+    at-scale parity tests) keeps the reference's contribution set on the fixtures, with T within
+    the reference's own log-cumsum rounding."""
+    d = gd.load(scene)
+    for v, cam in enumerate(d["cameras"]):
+        got = oracle.rasterize(d["gaussians"], cam, transmittance="product")
+        _cmp_wm(got, gd.weightmap(d, f"wm{v}_"))

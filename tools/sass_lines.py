@@ -69,10 +69,12 @@ def main():
     ap.add_argument("kernel")
     ap.add_argument("obj")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--sass-kernel", default=None,
+                    help="regex on the mangled name for nvdisasm (default: KERNEL_REGEX)")
     a = ap.parse_args()
     rows = sass_samples(a.report, a.kernel)
     with tempfile.TemporaryDirectory() as tmp:
-        name, seq = disasm_lines(cubin_of(a.obj, tmp), a.kernel)
+        name, seq = disasm_lines(cubin_of(a.obj, tmp), a.sass_kernel or a.kernel)
     print(f"kernel {name}: {len(rows)} profiled SASS instructions, {len(seq)} disassembled")
     if len(rows) != len(seq):
         print("WARNING: instruction counts differ; the object is not the profiled build")
