@@ -142,25 +142,69 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # inputs
 
-def make_inputs(cfgname, n_frames, log_prefix=""):
-    """Scene (host arrays) + dense tracks for frames 1..n_frames-1 (GPU tensors)."""
-    import torch
-
-    from paper_2604_02586_b200.engine import FrameEngine
-    from paper_2604_02586_b200.scene import generate_scene, oracle_tracks
+def make_scene(cfgname, n_frames, log_prefix=""):
+    """The restated generate_scene (numpy only) with the config's arguments."""
+    from paper_2604_02586_b200.scene import generate_scene
     c = CONFIGS[cfgname]
     seed, n, v = c["args"]
     t0 = time.time()
     scene = generate_scene(seed, n, v, n_frames, **c["kw"])
     log(f"{log_prefix}scene {cfgname}: N={n} V={v} frames={n_frames} in {time.time() - t0:.1f}s")
+    return scene
+
+
+def make_inputs(cfgname, n_frames, log_prefix="", frames=None):
+    """Scene (host arrays) + dense tracks (GPU oracle tracker) for the target frames `frames`
+    (default 1..n_frames-1) as GPU tensors."""
+    import torch
+
+    from paper_2604_02586_b200.engine import FrameEngine
+    from paper_2604_02586_b200.scene import oracle_tracks
+    scene = make_scene(cfgname, n_frames, log_prefix)
     t0 = time.time()
     eng = FrameEngine().bin(scene.frames[0], scene.cameras)
     tracks = {}
-    for f in range(1, n_frames):
+    for f in (range(1, n_frames) if frames is None else frames):
         tracks[f] = oracle_tracks(scene, f, engine=eng)
+    eng.plan.close()
     torch.cuda.synchronize()
     log(f"{log_prefix}tracks in {time.time() - t0:.1f}s")
     return scene, tracks
+
+
+def repo_libraries_mapped():
+    """In-repo shared objects mapped into this process (the reference arm must show only
+    oracle/liboracle.so)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths
+                  if os.path.realpath(p).startswith(os.path.realpath(ROOT)))
+
+
+def config_dict(cfgname, scene):
+    """The workload, identical in both arms' JSON lines."""
+    c = CONFIGS[cfgname]
+    seed, n, nv = c["args"]
+    w, h = scene.cameras[0].width, scene.cameras[0].height
+    return {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w, "height": h,
+            "scene": f"generate_scene(seed={seed}, {n}, {nv}, frames, "
+                     + ", ".join(f"{k}={v}" for k, v in c["kw"].items()) + ")",
+            "target_frame": f"frame 0 -> {c['gap']} (rank r: {c['gap']}*(r+1))",
+            "tracks": "oracle_track (scene.py:192-240), sigma 0, TRKF float32",
+            "step": "one frame: K1-K4 (rasterize + accumulate + solve per view, update_all)",
+            "l2": l2_note(n, nv, w, h)}
+
+
+def l2_note(n, nv, w, h):
+    trk, rec = 9 * nv * w * h / 1e6, 64 * n * nv / 1e6
+    if trk + rec > 126:
+        return (f"inputs larger than the 126 MB L2 (tracks {trk:.0f} MB, raster records "
+                f"{rec:.0f} MB per step); no flush")
+    return (f"inputs fit in the 126 MB L2 (tracks {trk:.1f} MB, raster records {rec:.1f} MB "
+            f"per step) and are not flushed between steps: a launch-bound config")
 
 
 def k2_bytes(n, v, w, h):
@@ -168,60 +212,41 @@ def k2_bytes(n, v, w, h):
 
 
 # ---------------------------------------------------------------------------------------------
-# CPU oracle baseline (bounded sample)
+# CPU arm (oracle/cpu_arm.py): the reference algorithm of the ★ path on the host cores
 
-def _cpu_view_task(args):
-    g, cam, target, valid = args
-    import oracle
-    t0 = time.perf_counter()
-    wm = oracle.rasterize(g, cam)
-    acc = oracle.accumulate(wm, target, valid, len(g))
-    sv = oracle.solve_view(acc)
-    return time.perf_counter() - t0, sv
+def cpu_frames(frame, cams, tgt, val, warmup, steps, log_prefix=""):
+    """Time `steps` whole frames (after `warmup`) of the CPU port in a pool over all host cores.
+    Returns a dict: per-step wall times, summed single-process CPU time, cores, tallies."""
+    from oracle import cpu_arm
+    t0 = time.time()
+    fr = cpu_arm.CpuFrame(frame, cams, tgt, val)
+    for _ in range(warmup):
+        fr.step()
+    walls, cpus = [], []
+    for _ in range(steps):
+        w_, c_ = fr.step()
+        walls.append(w_)
+        cpus.append(c_)
+    tallies = fr.tallies()
+    cores = fr.procs
+    fr.close()
+    log(f"{log_prefix}cpu frames: {warmup}+{steps} in {time.time() - t0:.1f}s "
+        f"(wall {np.mean(walls):.2f} s/frame, single-process {np.mean(cpus):.1f} s/frame)")
+    return dict(walls=walls, cpus=cpus, cores=cores, tallies=tallies,
+                model=cpu_arm.cpu_model(), host_cores=cpu_arm.host_cores())
 
 
-def cpu_baseline(scene, tracks, frame, n_views_sample, n_fuse_sample, procs):
-    """Time the oracle's ★ stages on a bounded sample: raster+accumulate+solve for
-    `n_views_sample` full views (process pool over views), update_all on `n_fuse_sample`
-    Gaussians; extrapolate to the full frame."""
-    import multiprocessing as mp
-
-    import oracle
-    oracle._lib()
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    g = scene.frames[0]
-    n = len(g)
-    cams = np.array([c.as_row() for c in scene.cameras])
-    nv = len(cams)
-    tgt, val = tracks[frame]
-    views = list(range(min(n_views_sample, nv)))
-    tasks = [(g, cams[v], tgt[v].cpu().numpy().astype(np.float64),
-              val[v].cpu().numpy().astype(bool)) for v in views]
-    t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(min(procs, len(tasks))) as pool:
-        res = pool.map(_cpu_view_task, tasks)
-    t_views = time.perf_counter() - t0
-    per_view = float(np.mean([r[0] for r in res]))
-    # fuse sample: all views' motions are needed; reuse sampled views' motions cyclically
-    sv = [r[1] for r in res]
-    mot = {k: np.stack([sv[v % len(sv)][k] for v in range(nv)]) for k in
-           ("status", "a", "b", "weight_sum", "pixel_count")}
-    idx = np.arange(min(n_fuse_sample, n))
-    sub = {k: mot[k][:, idx] for k in mot}
-    t0 = time.perf_counter()
-    oracle.update_all(g[idx], sub, cams)
-    t_fuse = (time.perf_counter() - t0) * (n / len(idx))
-    # full-frame single-process-equivalent times, and the pooled wall rate
-    cores = min(procs, len(tasks))
-    t_motion_wall = per_view * nv / cores
-    gv_s = n * nv / t_motion_wall
-    frames_s = 1.0 / (t_motion_wall + t_fuse / cores)
-    sample = (f"{len(views)} of {nv} views raster+accumulate+solve in full "
-              f"({per_view:.2f}s/view single-process, {cores} processes, pool wall "
-              f"{t_views:.1f}s), update_all on {len(idx)} of {n} Gaussians extrapolated")
-    return dict(value=gv_s, frames_per_s=frames_s, cores=cores, sample=sample,
-                t_view_s=per_view, t_fuse_frame_s=t_fuse)
+def cpu_baseline_dict(n, nv, res):
+    wall = float(np.mean(res["walls"]))
+    cpu = float(np.mean(res["cpus"]))
+    return {"value": n * nv / wall, "unit": "Gaussian-views/s", "cores": res["cores"],
+            "kind": "port", "cpu_model": res["model"],
+            "single_core_value": n * nv / cpu, "frames_per_s": 1.0 / wall,
+            "sample": f"{len(res['walls'])} whole frame(s) measured (all {nv} views "
+                      f"rasterize+accumulate+solve, update_all on all {n} Gaussians): "
+                      f"{wall:.2f} s wall per frame on {res['cores']} processes "
+                      f"({res['model']}), {cpu:.1f} s of single-process time per frame",
+            "tallies": res["tallies"]}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -243,7 +268,9 @@ def run_ours(args):
     frame = gap * (rank + 1)
     # every rank regenerates the (deterministic) scene; frame-0 Gaussians are then broadcast
     # from rank 0 over NCCL (once per clip), tracks are rank-local
-    scene, tracks = make_inputs(args.config, gap * world + 1, f"[rank {rank}] ")
+    # every rank regenerates the (deterministic) scene and tracks only its own target frame;
+    # frame-0 Gaussians are then broadcast from rank 0 over NCCL (once per clip)
+    scene, tracks = make_inputs(args.config, gap * world + 1, f"[rank {rank}] ", frames=[frame])
     w, h = scene.cameras[0].width, scene.cameras[0].height
     dev = torch.device("cuda", local)
     g_dev = torch.as_tensor(scene.frames[0], device=dev)
@@ -425,23 +452,19 @@ def run_ours(args):
         tallies = out.tallies()
         cpu = None
         if world == 1 and not args.no_cpu:
-            cb = cpu_baseline(scene, {frame: (tgt, val)}, frame, args.cpu_views,
-                              args.cpu_fuse, len(os.sched_getaffinity(0)))
-            cpu = {"value": cb["value"], "unit": "Gaussian-views/s", "cores": cb["cores"],
-                   "kind": "port", "sample": cb["sample"],
-                   "frames_per_s": cb["frames_per_s"]}
+            cams_rows = np.array([cm.as_row() for cm in cams])
+            res = cpu_frames(scene.frames[0], cams_rows, tgt.cpu().numpy(),
+                             val.cpu().numpy(), 0, args.cpu_frames)
+            cpu = cpu_baseline_dict(n, nv, res)
         line = {
             "metric": METRIC, "value": value, "unit": "Gaussian-views/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
-            "config": {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w,
-                       "height": h, "target_frame_per_rank": "gap*(rank+1)",
-                       "frames_per_s": world / (ms / 1e3),
-                       "parallelism": f"frame-sharded x{world}",
-                       "frames_in_flight": n_fly, "k2_ctas_per_sm_in_flight": k2_cap,
-                       "l2": f"inputs larger than the 126 MB L2 (tracks {9 * nv * w * h / 1e6:.0f} MB, "
-                             f"raster records {64 * n * nv / 1e6:.0f} MB per step); no flush"},
+            "config": config_dict(args.config, scene),
+            "frames_per_s": world / (ms / 1e3),
+            "parallelism": f"frame-sharded x{world}",
+            "frames_in_flight": n_fly, "k2_ctas_per_sm_in_flight": k2_cap,
             "e2e": {"value": n * nv * world / (ms_e2e / 1e3), "unit": "Gaussian-views/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": ms_e2e,
@@ -477,49 +500,34 @@ def run_ours(args):
 
 
 def run_reference(args):
-    """Reference arm: the CPU port of the reference algorithm (oracle/), all host cores."""
+    """Reference arm: the reference algorithm of the ★ path on the host cores (oracle/cpu_arm.py:
+    the C / numpy port pinned against the reference's own outputs), whole frames per step, with
+    inputs from the CPU oracle tracker -- the repo's CUDA library is never loaded here."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import torch
+    from oracle import cpu_arm
     c = CONFIGS[args.config]
     seed, n, nv = c["args"]
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-    scene, tracks = make_inputs(args.config, c["gap"] + 1)
-    frame = c["gap"]
-    procs = len(os.sched_getaffinity(0))
-    # Each step is a bounded CPU sample of several seconds; the repetitions are capped so the
-    # whole arm stays within ~3 minutes whatever --steps/--warmup ask for (the line reports the
-    # steps actually run).
-    budget_s, t_start = 180.0, time.time()
-    vals, done_warm = [], 0
-    for i in range(args.warmup + args.steps):
-        t0 = time.time()
-        cb = cpu_baseline(scene, tracks, frame, args.cpu_views, args.cpu_fuse, procs)
-        if i < args.warmup and done_warm < 1:
-            done_warm += 1
-        else:
-            vals.append(cb)
-        per = time.time() - t0
-        if len(vals) >= 1 and time.time() - t_start + per > budget_s:
-            break
-        if i + 1 >= done_warm + args.steps:
-            break
-    value = float(np.mean([v["value"] for v in vals]))
-    ms = n * nv / value * 1e3
-    w, h = scene.cameras[0].width, scene.cameras[0].height
-    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gaussian-views/s",
-            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": len(vals),
-            "warmup": done_warm, "steps_requested": args.steps, "ms_per_step": ms,
-            "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
-            "config": {"workload": c["name"], "n_gaussians": n, "n_views": nv, "width": w,
-                       "height": h},
-            "cpu_baseline": {"value": value, "unit": "Gaussian-views/s",
-                             "cores": vals[-1]["cores"], "kind": "port",
-                             "sample": vals[-1]["sample"]},
-            "e2e": {"value": value, "unit": "Gaussian-views/s", "h2d_bytes_per_step": 0,
+    scene = make_scene(args.config, c["gap"] + 1)
+    cams = np.array([cm.as_row() for cm in scene.cameras])
+    t0 = time.time()
+    tgt, val = cpu_arm.oracle_tracks(scene.frames[0], scene.frames[c["gap"]], cams, c["gap"])
+    log(f"CPU oracle tracks in {time.time() - t0:.1f}s")
+    res = cpu_frames(scene.frames[0], cams, tgt, val, args.warmup, args.steps)
+    cb = cpu_baseline_dict(n, nv, res)
+    wall = float(np.mean(res["walls"]))
+    return {"impl": "reference", "metric": METRIC, "value": cb["value"],
+            "unit": "Gaussian-views/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_scene + CPU oracle tracker, sigma 0)",
+            "config": config_dict(args.config, scene),
+            "frames_per_s": 1.0 / wall, "tallies": res["tallies"],
+            "step_wall_s": [round(x, 3) for x in res["walls"]],
+            "repo_libraries_mapped": repo_libraries_mapped(),
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "Gaussian-views/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
@@ -530,8 +538,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-views", type=int, default=8)
-    ap.add_argument("--cpu-fuse", type=int, default=3000)
+    ap.add_argument("--cpu-frames", type=int, default=1,
+                    help="whole frames timed for the cpu_baseline of the GPU arm")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_ours(args)

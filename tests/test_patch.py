@@ -56,3 +56,18 @@ def test_reference_typed_motions(gausstrack):
     st, a, b, w, c = motions_arrays(ref)
     np.testing.assert_array_equal(st, [1, 0, 1])
     np.testing.assert_array_equal(b[2], [4.0, 5.0])
+
+
+def test_reference_typed_inputs_convert(gausstrack):
+    """The shims receive the reference's own CameraView / Gaussian3D objects from
+    gausstrack.pipeline.compensate_frame: the host layout must accept them field by field."""
+    from gausstrack.core import CameraView, Gaussian3D
+
+    from paper_2604_02586_b200.core import cameras_array, gaussians_array
+    from tests import golden_data as gd
+    d = gd.load("scene21")
+    cams = [CameraView(c[:9].reshape(3, 3), c[9:12], c[12], c[13], c[14], c[15], int(c[16]),
+                       int(c[17])) for c in d["cameras"]]
+    np.testing.assert_array_equal(cameras_array(cams), d["cameras"])
+    gs = [Gaussian3D(r[0:3], r[3:7], r[7:10], r[10]) for r in d["gaussians"]]
+    np.testing.assert_array_equal(gaussians_array(gs), d["gaussians"])
