@@ -64,6 +64,9 @@ def _lib():
         lib.orc_accumulate.argtypes = [i64, ptr, ptr, ptr, ptr, ptr, ctypes.c_int, ctypes.c_int,
                                        ptr, ptr, i64, dbl, ptr, ptr, ptr, ptr, ptr, ptr]
         lib.orc_accumulate.restype = None
+        lib.orc_fit_hp.argtypes = [i64, ptr, ptr, ptr, ptr, ptr, ctypes.c_int, ptr, ptr, i64, dbl,
+                                   i64, dbl, ptr, ptr, ptr, ptr, ptr]
+        lib.orc_fit_hp.restype = None
         lib.orc_knn.argtypes = [i64, ptr, ctypes.c_int, ptr]
         lib.orc_knn.restype = None
         lib.orc_knn_queries.argtypes = [i64, ptr, ctypes.c_int, i64, ptr, ptr]
@@ -176,6 +179,27 @@ def accumulate(wm, target, valid, n_gaussians, static_threshold_px=1.0):
                           _p(scnt), _p(sws))
     return dict(v1=v1, v2=v2, weight_sum=ws, pixel_count=cnt, static_pixel_count=scnt,
                 static_weight_sum=sws)
+
+
+def fit_hp(wm, target, valid, n_gaussians, mu, det_floor=1e-12, min_pixels=3, min_weight=1e-3):
+    """accumulate_view + solve_view (motion2d.py:126-184) in long double around an anchor pixel:
+    the precision yardstick for at-scale fit comparisons (see orc_fit_hp).  mu: (N, 2) means.
+    Returns status (N,) int8, a (N,2,2), b (N,2), moved (N,2) = A mu + b."""
+    target = _c(target, np.float64)
+    valid = _c(valid, np.uint8)
+    w = valid.shape[1]
+    n = int(n_gaussians)
+    mu = _c(mu, np.float64).reshape(n, 2)
+    st = np.empty(n, np.int8)
+    a = np.empty((n, 2, 2))
+    b = np.empty((n, 2))
+    moved = np.empty((n, 2))
+    _lib().orc_fit_hp(len(wm["pixel_x"]), _p(_c(wm["pixel_x"], np.int32)),
+                      _p(_c(wm["pixel_y"], np.int32)), _p(_c(wm["gaussian_id"], np.int64)),
+                      _p(_c(wm["alpha"], np.float64)), _p(_c(wm["transmittance"], np.float64)), w,
+                      _p(target), _p(valid), n, det_floor, int(min_pixels), min_weight, _p(mu),
+                      _p(st), _p(a), _p(b), _p(moved))
+    return dict(status=st, a=a, b=b, moved=moved)
 
 
 # ---------------------------------------------------------------------------

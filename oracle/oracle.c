@@ -400,3 +400,91 @@ void orc_knn_queries(int64_t n, const double *pos, int kk, int64_t nq, const int
 void orc_knn(int64_t n, const double *pos, int kk, int64_t *adj) {
   orc_knn_queries(n, pos, kk, n, NULL, adj);
 }
+
+/* High-precision reference for at-scale comparisons of the per-view fits (accumulate_view +
+ * solve_view, motion2d.py:126-184): moments in long double (x87, 64-bit mantissa) around an
+ * anchor pixel per Gaussian (its first contribution; the translation is exact algebra), 3x3 solve
+ * by partial-pivot elimination in long double, b mapped back to absolute pixels.  The
+ * reference's own fp64 sums of absolute pixel moments have condition numbers of 1e10-1e14
+ * (SURVEY §7), so at scale it is the less accurate side; this restatement is the yardstick both
+ * the GPU and the fp64 restatement are measured against.  Outputs per Gaussian: status
+ * (count >= min_pixels && sum w >= min_weight && det >= det_floor), a (2x2), b (2), and the
+ * moved mean A mu + b of the given 2D means mu (N, 2). */
+void orc_fit_hp(int64_t m, const int32_t *px, const int32_t *py, const int64_t *gid,
+                const double *alpha, const double *trans, int W, const double *target,
+                const uint8_t *valid, int64_t n, double det_floor, int64_t min_pixels,
+                double min_weight, const double *mu, int8_t *status, double *a_out,
+                double *b_out, double *moved_out) {
+  long double *acc = (long double *)calloc((size_t)n * 15, sizeof(long double));
+  int64_t *cnt = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+  int32_t *anc = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)(n > 0 ? n : 1));
+  for (int64_t k = 0; k < m; k++) {
+    int64_t pix = (int64_t)py[k] * W + px[k];
+    if (!valid[pix]) continue;
+    int64_t g = gid[k];
+    if (cnt[g] == 0) {
+      anc[2 * g] = px[k];
+      anc[2 * g + 1] = py[k];
+    }
+    long double w = (long double)alpha[k] * (long double)trans[k];
+    long double x = (long double)(px[k] - anc[2 * g]), y = (long double)(py[k] - anc[2 * g + 1]);
+    long double u = target[2 * pix], v = target[2 * pix + 1];
+    long double *A = acc + 15 * g;
+    A[0] += w; A[1] += w * x; A[2] += w * y; A[3] += w * x * x; A[4] += w * x * y;
+    A[5] += w * y * y; A[6] += w * u; A[7] += w * v; A[8] += w * x * u; A[9] += w * x * v;
+    A[10] += w * y * u; A[11] += w * y * v;
+    cnt[g]++;
+  }
+  for (int64_t g = 0; g < n; g++) {
+    long double *A = acc + 15 * g;
+    /* h = [x, y, 1]: V1 = [[Sxx Sxy Sx] [Sxy Syy Sy] [Sx Sy S]], V2 rows h_i * [u v] */
+    long double M[3][5] = {{A[3], A[4], A[1], A[8], A[9]},
+                           {A[4], A[5], A[2], A[10], A[11]},
+                           {A[1], A[2], A[0], A[6], A[7]}};
+    long double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                      M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                      M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    int ok = cnt[g] >= min_pixels && A[0] >= (long double)min_weight &&
+             det >= (long double)det_floor;
+    status[g] = (int8_t)ok;
+    double *ao = a_out + 4 * g, *bo = b_out + 2 * g, *mo = moved_out + 2 * g;
+    if (!ok) {
+      ao[0] = 1; ao[1] = 0; ao[2] = 0; ao[3] = 1; bo[0] = bo[1] = 0;
+      mo[0] = mu[2 * g];
+      mo[1] = mu[2 * g + 1];
+      continue;
+    }
+    for (int c = 0; c < 3; c++) {
+      int p = c;
+      for (int r = c + 1; r < 3; r++)
+        if (fabsl(M[r][c]) > fabsl(M[p][c])) p = r;
+      if (p != c)
+        for (int j = 0; j < 5; j++) {
+          long double t = M[c][j]; M[c][j] = M[p][j]; M[p][j] = t;
+        }
+      for (int r = c + 1; r < 3; r++) {
+        long double f = M[r][c] / M[c][c];
+        for (int j = c; j < 5; j++) M[r][j] -= f * M[c][j];
+      }
+    }
+    long double X[3][2];
+    for (int rhs = 0; rhs < 2; rhs++)
+      for (int r = 2; r >= 0; r--) {
+        long double s = M[r][3 + rhs];
+        for (int j = r + 1; j < 3; j++) s -= M[r][j] * X[j][rhs];
+        X[r][rhs] = s / M[r][r];
+      }
+    /* X = [A^T; b_a^T] in anchored coordinates: x' = A (x - anc) + b_a */
+    long double a00 = X[0][0], a01 = X[1][0], a10 = X[0][1], a11 = X[1][1];
+    long double ax = anc[2 * g], ay = anc[2 * g + 1];
+    long double b0 = X[2][0] - (a00 * ax + a01 * ay), b1 = X[2][1] - (a10 * ax + a11 * ay);
+    ao[0] = (double)a00; ao[1] = (double)a01; ao[2] = (double)a10; ao[3] = (double)a11;
+    bo[0] = (double)b0; bo[1] = (double)b1;
+    long double mx = mu[2 * g], my = mu[2 * g + 1];
+    mo[0] = (double)(a00 * mx + a01 * my + b0);
+    mo[1] = (double)(a10 * mx + a11 * my + b1);
+  }
+  free(acc);
+  free(cnt);
+  free(anc);
+}
