@@ -109,9 +109,9 @@ def test_counts_and_motions_at_scale(run):
         hp_err = np.abs(got_moved - hp["moved"])[hp_both]
         report["gpu_vs_hp"] = dict(status_flips=int((st_all[sl] != hp["status"]).sum()),
                                    moved_mean_max_px=float(hp_err.max()) if hp_err.size else 0.0,
-                                   over_1um=int((hp_err.max(axis=1) > 1e-6).sum()))
+                                   n_over_tol=int((hp_err.max(axis=1) > 1e-6).sum()))
         assert report["gpu_vs_hp"]["status_flips"] <= max(1, 1e-4 * n)
-        assert report["gpu_vs_hp"]["over_1um"] <= max(1, 1e-5 * hp_both.sum()), report
+        assert report["gpu_vs_hp"]["n_over_tol"] <= max(1, 1e-5 * hp_both.sum()), report
         for mode in ("product", "reference"):
             wm = wm_p if mode == "product" else oracle.rasterize(g, cams[v], transmittance=mode)
             acc = oracle.accumulate(wm, tgt, val, n)
