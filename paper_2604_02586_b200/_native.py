@@ -257,6 +257,7 @@ class Plan:
         h = ctypes.c_void_p()
         check(self._lib.ts_plan_create(ctypes.byref(h)), "ts_plan_create")
         self.handle = h
+        self.k2_ctas_per_sm = 0
 
     def close(self):
         if self.handle:
@@ -279,6 +280,7 @@ class Plan:
         """Cap the persistent K2 grid at `ctas_per_sm` CTAs per SM (0: full residency)."""
         check(self._lib.ts_plan_set_k2_ctas_per_sm(self.handle, int(ctas_per_sm)),
               "ts_plan_set_k2_ctas_per_sm")
+        self.k2_ctas_per_sm = int(ctas_per_sm)
 
     def timing_read(self):
         tot = (ctypes.c_double * N_STAGES)()

@@ -23,6 +23,7 @@
 //     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
 //     bit-reproducible (K3 adds the sub-slots in fixed order).
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -421,6 +422,297 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
     for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);
 }
 
+// ---------------------------------------------------------------------------------------------
+// K2 accumulate mode: batched evaluation (the production path).
+//
+// Same work units, culling and arithmetic as k2_raster, but the culled Gaussians of a unit are
+// appended (in depth order) to a per-warp batch of K2B_BATCH entries in shared memory (SoA), and a
+// full batch is processed pixel-parallel: each lane holds, for each of its two pixels, the bit mask
+// of batch entries whose bbox covers it, and walks those entries front to back.  Two candidates
+// per lane per trip (from either pixel's list) have their alphas evaluated independently -- alpha
+// does not depend on T -- and are then composited in order into the pixel's T.  A warp trip thus
+// evaluates up to 64 (Gaussian, pixel) pairs instead of one Gaussian's 64 pixel slots, so the
+// fp64 lanes are busy with candidates rather than bbox padding.  The moments of the batch's
+// entries are then reduced by two lanes per entry (alternate contributing pixels, one xor
+// shuffle), each entry's (gv, quadrant) slot written once.  Arithmetic per pair is the same as
+// k2_raster (q in numpy's order, table exp, T as the running product), so the contribution set,
+// alpha, T and the integer counts are bit-identical to it; only the summation order of the
+// moments differs.
+constexpr int K2B_BATCH = 16;   // entries per batch (two flush lanes each)
+constexpr int K2B_WARPS = 4;
+
+template <typename TrackT>
+struct K2BWarp {
+  double mx[K2B_BATCH], my[K2B_BATCH], i00[K2B_BATCH], i01x2[K2B_BATCH], i11[K2B_BATCH],
+      op[K2B_BATCH];
+  uint64_t rect[K2B_BATCH];
+  uint32_t slot[K2B_BATCH];
+  int ax[K2B_BATCH], ay[K2B_BATCH];
+  double w[K2B_BATCH][K2_WROW];
+  TrackT trk_u[64], trk_v[64];
+};
+
+// alpha of one batch entry at one pixel; pass = q <= 9 && alpha >= cutoff (splat.py:153-155)
+template <typename TrackT>
+__device__ __forceinline__ double k2b_alpha(const K2BWarp<TrackT> &S, int k, double fpx,
+                                            double fpy, double cutoff, const double *etab,
+                                            bool &pass) {
+  const double dx = sub(fpx, S.mx[k]), dy = sub(fpy, S.my[k]);
+  const double q = add(add(mul(mul(S.i00[k], dx), dx), mul(mul(S.i01x2[k], dx), dy)),
+                       mul(mul(S.i11[k], dy), dy));
+  const bool in = q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS;
+  const double a = alpha_of_table(S.op[k], in ? q : 0.0, etab);  // table index stays in range
+  pass = in && a >= cutoff;
+  return a;
+}
+
+template <typename TrackT>
+__device__ __forceinline__ void k2b_process(K2BWarp<TrackT> &S, const K2Params &P, int lane,
+                                            int nb, double fpx, double fpy0, double fpy1,
+                                            bool valid0, bool valid1, double &T0, double &T1,
+                                            uint64_t &done64, uint64_t static64, int qx0,
+                                            int qy0, const double *etab) {
+  __syncwarp();
+  const double es = P.early_stop, cutoff = P.alpha_cutoff;
+  // candidate entries of each of the lane's pixels (bit k = entry k, depth order)
+  uint32_t mA = 0, mB = 0;
+  for (int k = 0; k < nb; k++) {
+    const uint64_t r = S.rect[k];
+    mA |= (uint32_t)((r >> lane) & 1ull) << k;
+    mB |= (uint32_t)((r >> (lane + 32)) & 1ull) << k;
+  }
+  if (!(T0 >= es)) mA = 0;
+  if (!(T1 >= es)) mB = 0;
+  uint32_t cA = 0, cB = 0;  // entries with a tracked contribution at the pixel
+  while (__any_sync(0xffffffffu, (mA | mB) != 0u)) {
+    // two candidates per trip: the next of pixel A and the next of pixel B; when one list is
+    // empty both come from the other (in order: alpha is independent of T)
+    int k1 = -1, k2 = -1;
+    bool b1 = false, b2 = false;
+    if (mA) {
+      k1 = __ffs(mA) - 1;
+      mA &= mA - 1;
+    } else if (mB) {
+      k1 = __ffs(mB) - 1;
+      mB &= mB - 1;
+      b1 = true;
+    }
+    if (mB) {
+      k2 = __ffs(mB) - 1;
+      mB &= mB - 1;
+      b2 = true;
+    } else if (mA) {
+      k2 = __ffs(mA) - 1;
+      mA &= mA - 1;
+    }
+    bool pass1 = false, pass2 = false;
+    double a1 = 0.0, a2 = 0.0;
+    if (k1 >= 0) a1 = k2b_alpha(S, k1, fpx, b1 ? fpy1 : fpy0, cutoff, etab, pass1);
+    if (k2 >= 0) a2 = k2b_alpha(S, k2, fpx, b2 ? fpy1 : fpy0, cutoff, etab, pass2);
+    // composite in depth order (k1 before k2 when both are the same pixel's)
+    if (pass1) {
+      const double tin = b1 ? T1 : T0;
+      if (tin >= es) {
+        const double tout = mul(tin, sub(1.0, a1));
+        if (b1) T1 = tout; else T0 = tout;
+        if (b1 ? valid1 : valid0) {
+          S.w[k1][b1 ? lane + 32 : lane] = mul(a1, tin);  // motion2d.py:151
+          if (b1) cB |= 1u << k1; else cA |= 1u << k1;
+        }
+      }
+    }
+    if (pass2) {
+      const double tin = b2 ? T1 : T0;
+      if (tin >= es) {
+        const double tout = mul(tin, sub(1.0, a2));
+        if (b2) T1 = tout; else T0 = tout;
+        if (b2 ? valid1 : valid0) {
+          S.w[k2][b2 ? lane + 32 : lane] = mul(a2, tin);
+          if (b2) cB |= 1u << k2; else cA |= 1u << k2;
+        }
+      }
+    }
+    if (!(T0 >= es)) mA = 0;  // saturated: the pixel's later entries are all cut
+    if (!(T1 >= es)) mB = 0;
+  }
+  done64 = (uint64_t)__ballot_sync(0xffffffffu, !(T0 >= es)) |
+           ((uint64_t)__ballot_sync(0xffffffffu, !(T1 >= es)) << 32);
+  // per-entry contribution masks, kept by the entry's two flush lanes (lane & 15)
+  const int e = lane & (K2B_BATCH - 1), h = lane / K2B_BATCH;
+  uint64_t cm = 0;
+  for (int k = 0; k < nb; k++) {
+    const uint64_t mk = (uint64_t)__ballot_sync(0xffffffffu, (cA >> k) & 1u) |
+                        ((uint64_t)__ballot_sync(0xffffffffu, (cB >> k) & 1u) << 32);
+    if (e == k) cm = mk;
+  }
+  __syncwarp();
+  // moments (motion2d.py:144-160) anchored at the entry's bbox centre pixel: lane h of entry e
+  // sums its (h-th, h+2-th, ...) contributing pixels, one xor shuffle adds the two halves
+  double m[TS_NMOM];
+#pragma unroll
+  for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
+  uint32_t cnt = 0, scnt = 0;
+  if (cm) {
+    const int ax = S.ax[e], ay = S.ay[e];
+    const double fax = (double)ax, fay = (double)ay;
+    const double bx = (double)(qx0 - ax), by = (double)(qy0 - ay);
+    uint64_t bits = cm;
+    if (h) bits &= bits - 1;
+    while (bits) {
+      const int p = __ffsll((long long)bits) - 1;
+      bits &= bits - 1;
+      bits &= bits - 1;
+      const double w = S.w[e][p];
+      const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
+      const double ua = (double)S.trk_u[p] - fax, va = (double)S.trk_v[p] - fay;
+      const double wx = w * dx, wy = w * dy;
+      m[0] += w;
+      m[1] += wx;
+      m[2] += wy;
+      m[3] += wx * dx;
+      m[4] += wx * dy;
+      m[5] += wy * dy;
+      m[6] += w * ua;
+      m[7] += w * va;
+      m[8] += wx * ua;
+      m[9] += wx * va;
+      m[10] += wy * ua;
+      m[11] += wy * va;
+      const bool st = (static64 >> p) & 1ull;
+      m[12] += st ? w : 0.0;
+      scnt += st;
+      cnt++;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], K2B_BATCH);
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, K2B_BATCH);
+  scnt += __shfl_xor_sync(0xffffffffu, scnt, K2B_BATCH);
+  if (cm && e < nb) {
+    Partial *dst = P.partial + S.slot[e];
+    if (h == 0) {
+      dst->m[0] = m[0]; dst->m[1] = m[1]; dst->m[2] = m[2]; dst->m[3] = m[3];
+      dst->m[4] = m[4]; dst->m[5] = m[5]; dst->m[6] = m[6];
+    } else {
+      dst->m[7] = m[7]; dst->m[8] = m[8]; dst->m[9] = m[9]; dst->m[10] = m[10];
+      dst->m[11] = m[11]; dst->m[12] = m[12];
+      dst->count = cnt;
+      dst->static_count = scnt;
+      P.flag[S.slot[e]] = 1;
+    }
+  }
+  __syncwarp();
+}
+
+template <typename TrackT>
+__global__ void __launch_bounds__(K2B_WARPS * 32) k2_accum(const K2Params P) {
+  extern __shared__ __align__(16) unsigned char k2_smem_raw[];
+  double *etab = reinterpret_cast<double *>(k2_smem_raw);  // exp(-k/64), k = 0..288
+  for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  K2BWarp<TrackT> &S = reinterpret_cast<K2BWarp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
+  const uint32_t n_units = 4u * *P.n_items;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  for (;;) {
+    uint32_t unit = 0;
+    if (lane == 0) unit = atomicAdd(P.work_counter, 1u);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= n_units) break;
+    const int tile = (int)P.items[unit >> 2];
+    const int quad = (int)(unit & 3);
+    const uint32_t start = P.tile_range[2 * tile], end = P.tile_range[2 * tile + 1];
+    const int v = tile / P.tiles_per_view;
+    const int t = tile - v * P.tiles_per_view;
+    const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
+    const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 8;
+    const int px = qx0 + (lane & 7);
+    const int py0 = qy0 + (lane >> 3), py1 = py0 + 4;
+    const double fpx = (double)px, fpy0 = (double)py0, fpy1 = (double)py1;
+    const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
+
+    bool valid0 = false, valid1 = false;
+    uint64_t static64 = 0;
+    __syncwarp();
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      const int py = hh ? py1 : py0;
+      TrackT u = TrackT(0), vv = TrackT(0);
+      bool val = false;
+      if (hh ? in1 : in0) {
+        // plain loads (no read-only path): the tracks may be pinned host memory read in place
+        const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
+        const uint8_t vb = P.track_valid[pix];
+        const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
+        const TrackT tu = tg[0], tv = tg[1];
+        val = vb != 0;
+        if (val) {  // invalid targets may be NaN: never used
+          u = tu;
+          vv = tv;
+        }
+      }
+      const int p = lane + 32 * hh;
+      S.trk_u[p] = u;
+      S.trk_v[p] = vv;
+      const bool st = val && is_static((double)u, (double)vv, px, py, P.static_thr);
+      static64 |= (uint64_t)__ballot_sync(0xffffffffu, st) << (32 * hh);
+      if (hh) valid1 = val; else valid0 = val;
+    }
+    double T0 = in0 ? 1.0 : 0.0, T1 = in1 ? 1.0 : 0.0;
+    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, !(T0 >= P.early_stop)) |
+                      ((uint64_t)__ballot_sync(0xffffffffu, !(T1 >= P.early_stop)) << 32);
+    int nb = 0;  // entries in the batch
+    for (uint32_t b = start; b < end; b += 32) {
+      if (done64 == ~0ull) break;
+      const uint32_t i = b + lane;
+      bool hit = false;
+      RasterRec r;
+      uint64_t rect = 0;
+      uint32_t ibase = 0;
+      if (i < end) {
+        const uint32_t gv = P.inst_gv[i];
+        ibase = __ldg(P.inst_base + gv);
+        r = P.rec[gv];
+        rect = quad_rect(r, qx0, qy0);
+        hit = (rect & ~done64) != 0ull;
+      }
+      uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      while (hm) {
+        // append the first (K2B_BATCH - nb) remaining hits, in instance order
+        const int take = min(K2B_BATCH - nb, __popc(hm));
+        const int rank = __popc(hm & lt_mask);
+        const bool mine = ((hm >> lane) & 1u) && rank < take;
+        if (mine) {
+          const int k = nb + rank;
+          S.mx[k] = r.mx;
+          S.my[k] = r.my;
+          S.i00[k] = r.i00;
+          S.i01x2[k] = r.i01x2;
+          S.i11[k] = r.i11;
+          S.op[k] = r.opacity;
+          S.rect[k] = rect;
+          const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
+          S.slot[k] = ibase + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
+                                         ((qx0 >> 3) - bx0));
+          S.ax[k] = anchor_x(r);
+          S.ay[k] = anchor_y(r);
+        }
+        hm &= ~__ballot_sync(0xffffffffu, mine);
+        nb += take;
+        if (nb == K2B_BATCH) {
+          k2b_process(S, P, lane, nb, fpx, fpy0, fpy1, valid0, valid1, T0, T1, done64, static64,
+                      qx0, qy0, etab);
+          nb = 0;
+        }
+      }
+    }
+    if (nb > 0)
+      k2b_process(S, P, lane, nb, fpx, fpy0, fpy1, valid0, valid1, T0, T1, done64, static64, qx0,
+                  qy0, etab);
+  }
+}
+
 // Compact list of the non-empty tiles in [t0, t1) (order irrelevant: every unit is independent).
 __global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, int t1,
                                uint32_t *__restrict__ items, uint32_t *__restrict__ n_items) {
@@ -486,6 +778,22 @@ static cudaError_t launch_mode(const K2Params &P, cudaStream_t s, int cap) {
   return cudaGetLastError();
 }
 
+template <typename TrackT>
+static cudaError_t launch_accum(const K2Params &P, cudaStream_t s, int cap) {
+  auto kern = k2_accum<TrackT>;
+  const size_t smem = K2_ETAB_BYTES + sizeof(K2BWarp<TrackT>) * K2B_WARPS;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2B_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (cap > 0 && cap < per_sm) per_sm = cap;
+  kern<<<sms * (per_sm > 0 ? per_sm : 1), K2B_WARPS * 32, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uint32_t *inst_gv,
                       const uint32_t *tile_range, const uint32_t *inst_base, uint32_t *items,
                       uint32_t *counters, int tile_begin, int tile_end, const void *track_target,
@@ -545,8 +853,13 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.dom_depth = dom_depth;
   P.stats = stats;
   if (mode == K2_ACCUMULATE) {
-    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
-    return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
+    static const bool legacy = std::getenv("TS_K2_LEGACY") != nullptr;  // A/B of the old loop
+    if (legacy) {
+      if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
+      return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
+    }
+    if (track_dtype == TS_TRACK_F32) return launch_accum<float>(P, s, ctas_per_sm);
+    return launch_accum<double>(P, s, ctas_per_sm);
   }
   if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s, ctas_per_sm);
   return launch_mode<K2_DOMINANT, float>(P, s, ctas_per_sm);

@@ -26,11 +26,24 @@ def frames_for_rank(target_frames, rank, world):
     return [f for i, f in enumerate(target_frames) if i % world == rank]
 
 
+def collective_device(group=None):
+    """The device collectives of `group` run on: the current CUDA device for NCCL (which cannot
+    move host tensors), the CPU otherwise (gloo)."""
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def broadcast_rows(rows, group=None, src=0, device=None):
-    """Broadcast the (N, 11) float64 Gaussian rows of the clip's first frame from `src`."""
+    """Broadcast the (N, 11) float64 Gaussian rows of the clip's first frame from `src`
+    (on `device`, default: the group's collective device)."""
     import torch
     import torch.distributed as dist
     t = rows if isinstance(rows, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(rows))
+    if device is None and dist.is_initialized():
+        device = collective_device(group)
     if device is not None:
         t = t.to(device)
     t = t.contiguous()
@@ -54,11 +67,11 @@ def gather_frames(local, n_rows, target_frames, group=None, dst=0):
     rank = dist.get_rank(group)
     per_rank = [frames_for_rank(target_frames, r, world) for r in range(world)]
     slots = max(len(p) for p in per_rank)
-    any_t = next(iter(local.values())) if local else None
-    device = any_t.device if any_t is not None else torch.device("cpu")
+    # every rank (including one that owns no frame) uses the group's collective device
+    device = collective_device(group)
     buf = torch.zeros((slots, n_rows, 11), dtype=torch.float64, device=device)
     for i, f in enumerate(per_rank[rank]):
-        buf[i] = local[f]
+        buf[i] = torch.as_tensor(local[f]).to(device)
     out = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
     dist.gather(buf, out, dst=dst, group=group)
     if rank != dst:

@@ -151,6 +151,26 @@ class FrameEngine:
             static_pixel_count=torch.empty(nv, dtype=torch.int32, device=dev),
             static_weight_sum=torch.empty(nv, **f64))
 
+    def outputs_fit(self, out: FrameOutputs) -> bool:
+        """True if `out` has this engine's shapes (N Gaussians, N x V fits) on its device."""
+        n, nv = self.n, self.n * self.n_views
+        dev = self._gauss.device
+        want = dict(delta_mean=(n, 3), rotation=(n, 4), scale=(n, 3), status=(n,),
+                    motion_status=(nv,), motion_a=(nv, 2, 2), motion_b=(nv, 2),
+                    weight_sum=(nv,), pixel_count=(nv,), static_pixel_count=(nv,),
+                    static_weight_sum=(nv,))
+        for k, shape in want.items():
+            t = getattr(out, k)
+            if tuple(t.shape) != shape or t.device != dev or not t.is_contiguous():
+                return False
+        return True
+
+    def check_outputs(self, out: FrameOutputs):
+        """Reject a caller's output buffers that the kernels would overrun."""
+        if not self.outputs_fit(out):
+            raise ValueError(f"output buffers do not match this engine's binning "
+                             f"(N={self.n}, views={self.n_views}); use alloc_outputs()")
+
     def compensate(self, track_target, track_valid, out: FrameOutputs | None = None,
                    stream=None) -> FrameOutputs:
         """Fused raster-accumulate, per-view affine fit and multi-view fuse for one frame."""
@@ -183,6 +203,8 @@ class FrameEngine:
         dtype = nat.TS_TRACK_F32 if tgt.dtype == torch.float32 else nat.TS_TRACK_F64
         if out is None:
             out = self.alloc_outputs()
+        else:
+            self.check_outputs(out)
         m = nat.Motions(nat.dptr(out.motion_status).value, nat.dptr(out.motion_a).value,
                         nat.dptr(out.motion_b).value, nat.dptr(out.weight_sum).value,
                         nat.dptr(out.pixel_count).value, nat.dptr(out.static_pixel_count).value,
@@ -238,17 +260,22 @@ class StreamingEngine:
     # the full grid)
     K2_CTAS_PER_SM = 3
 
+    SWITCH_VOTES = 3  # consecutive steps that must favour the other mode before "auto" switches
+
     def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
         torch = _torch()
-        self._compute_ms = None  # median of the last step periods ("auto" mode)
+        self._compute_ms = None  # median of the last in-place step periods ("auto" mode)
         self._periods = []
         self._last_zero_copy = True
+        self._votes = 0
         self._burst = 0
         self.steps_zero_copy = 0  # steps whose tracks were read in place / copied whole
         self.steps_full_copy = 0
         self._timing = []  # (start, end) events of computed steps not yet read
         self.engines = [engine if engine is not None else FrameEngine()] + \
             [FrameEngine() for _ in range(self.N_ENGINES - 1)]
+        # the K2 cap applies while this streamer runs; close() restores a passed-in engine's
+        self._caller_cap = engine.plan.k2_ctas_per_sm if engine is not None else None
         for e_ in self.engines:
             e_.plan.set_k2_ctas_per_sm(self.K2_CTAS_PER_SM)
         self.zero_copy_tracks = zero_copy_tracks
@@ -277,6 +304,9 @@ class StreamingEngine:
         shapes = (tuple(g_host.shape), tuple(t_host.shape), tuple(v_host.shape), t_host.dtype,
                   tracks)
         if s is None or s[0] != shapes:
+            if s is not None and self._free[i] is not None:
+                # the old buffers go back to the caching allocator: no stream may still use them
+                self._free[i].synchronize()
             dev = torch.device("cuda", torch.cuda.current_device())
             s = (shapes, torch.empty(g_host.shape, dtype=torch.float64, device=dev),
                  torch.empty(t_host.shape, dtype=t_host.dtype, device=dev) if tracks else None,
@@ -303,11 +333,16 @@ class StreamingEngine:
         # the binning does not touch the outputs: only K2-K4 wait for their previous D2H
         if self._out_free[e] is not None:
             cs.wait_event(self._out_free[e])
+        if self._outs[e] is not None and not eng.outputs_fit(self._outs[e]):
+            if self._out_free[e] is not None:
+                self._out_free[e].synchronize()  # shapes changed: reallocate after the last D2H
+            self._outs[e] = None
         out = eng.compensate(t_d, v_d, self._outs[e], stream=cs)
         self._outs[e] = out
         computed = torch.cuda.Event(enable_timing=True)
         computed.record(cs)
-        self._timing.append((t0, computed, self._burst))
+        if self.zero_copy_tracks == "auto":
+            self._timing.append((t0, computed, self._burst, t_d is not None and _pinned(t_d)))
         self._free[i] = computed
         ds = self.d2h_stream
         ds.wait_event(computed)
@@ -354,24 +389,34 @@ class StreamingEngine:
     def _choose_zero_copy(self, g_host, t_host, v_host):
         if self.zero_copy_tracks != "auto":
             return bool(self.zero_copy_tracks)
-        # fold in the step period (interval between consecutive finished steps; never blocks):
-        # copying the whole arrays pays off when that copy fits under the period
-        # (over two steps: consecutive steps finish on alternating compute streams)
-        while len(self._timing) >= 3 and self._timing[2][1].query():
-            prev, cur = self._timing.pop(0), self._timing[1]
-            if prev[2] != cur[2]:  # the two steps straddle a flush (caller's idle time)
-                continue
-            self._periods = (self._periods + [0.5 * prev[1].elapsed_time(cur[1])])[-5:]
+        # Fold in the step period (interval between consecutive finished steps; never blocks).
+        # Only periods of steps that read the tracks in place count: a full-copy step's period
+        # contains the copy itself, which would make the copy look affordable (self-reinforcing).
+        # Steps finish on N_ENGINES compute streams, so a period is read once every event of
+        # the window has completed.
+        k = self.N_ENGINES
+        while len(self._timing) > k and all(t[1].query() for t in self._timing[:k + 1]):
+            first, last = self._timing[0], self._timing[k]
+            window = self._timing[:k + 1]
+            self._timing.pop(0)
+            if first[2] != last[2] or not all(t[3] for t in window):
+                continue  # straddles a flush (caller's idle time) or includes a full copy
+            self._periods = (self._periods + [first[1].elapsed_time(last[1]) / k])[-5:]
             self._compute_ms = sorted(self._periods)[len(self._periods) // 2]  # robust median
         if self._compute_ms is None:
-            return True
+            return self._last_zero_copy
         copy_ms = (g_host.numel() * g_host.element_size() + t_host.numel() *
                    t_host.element_size() + v_host.numel()) / (self.H2D_GBS * 1e6)
-        # hysteresis: leave the current mode only on a clear margin
-        if self._last_zero_copy:
-            self._last_zero_copy = not copy_ms < 0.85 * self._compute_ms
+        # the copy pays off when it hides under the in-place step period; switching needs
+        # SWITCH_VOTES consecutive steps on the other side of a margin (hysteresis)
+        want_zero_copy = not copy_ms < (0.85 if self._last_zero_copy else 0.95) * self._compute_ms
+        if want_zero_copy == self._last_zero_copy:
+            self._votes = 0
         else:
-            self._last_zero_copy = copy_ms > 0.95 * self._compute_ms
+            self._votes += 1
+            if self._votes >= self.SWITCH_VOTES:
+                self._last_zero_copy = want_zero_copy
+                self._votes = 0
         return self._last_zero_copy
 
     def flush(self):
@@ -380,6 +425,13 @@ class StreamingEngine:
         done = self._compute(prev) if prev is not None else None
         self._burst += 1  # a period across this point would span the caller's idle time
         return done
+
+    def close(self):
+        """Restore a passed-in engine's K2 residency cap and release the extra engines."""
+        if self._caller_cap is not None:
+            self.engines[0].plan.set_k2_ctas_per_sm(self._caller_cap)
+        for e_ in self.engines[1:]:
+            e_.plan.close()
 
     def wait_all(self, stream):
         """Make `stream` wait for every result copy issued so far."""

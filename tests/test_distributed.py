@@ -115,3 +115,32 @@ def test_run_pipeline_result_sharing(tmp_path):
             np.testing.assert_array_equal(got[str(f)], np.full((6, 11), float(f)) + np.arange(11))
         np.testing.assert_array_equal(got["tallies"], [1, 2, 3, 4, 5])
         np.testing.assert_array_equal(got["src"], [0] * 5)
+
+
+def _idle_rank_worker(rank, world, port, out_path):
+    """world > number of target frames: rank 2 owns none and still joins the gather."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows, cams, tracks = _scene()
+    first = torch.as_tensor(rows) if rank == 0 else torch.zeros(rows.shape, dtype=torch.float64)
+    targets = (1, 2)
+    mine = {f: tracks[f] for f in frames_for_rank(targets, rank, world)}
+    res = compensate_clip_sharded(first, cams, mine, targets, compute=_cpu_compute)
+    if rank == 0:
+        np.savez(out_path, **{str(f): v.numpy() for f, v in res.items()})
+    else:
+        assert res is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_sharded_with_idle_rank(tmp_path):
+    rows, cams, tracks = _scene()
+    out = tmp_path / "idle.npz"
+    mp.spawn(_idle_rank_worker, args=(3, _free_port(), str(out)), nprocs=3, join=True)
+    got = np.load(out)
+    assert sorted(int(k) for k in got.files) == [1, 2]
+    for f in (1, 2):
+        serial = _cpu_compute(torch.as_tensor(rows), cams, *tracks[f]).numpy()
+        np.testing.assert_array_equal(got[str(f)], serial)

@@ -12,8 +12,18 @@ pytestmark = pytest.mark.gpu
 from tests import golden_data as gd  # noqa: E402
 
 
+def _direct_rows(direct, g, cams, t, v):
+    direct.bin(g, cams)
+    o = direct.compensate(t, v)
+    return torch.cat([o.delta_mean, o.rotation, o.scale,
+                      o.status.to(torch.float64)[:, None]], 1).cpu()
+
+
 @pytest.mark.parametrize("zero_copy", [True, False, "auto"])
 def test_streaming_matches_direct(zero_copy):
+    """2 * N_SLOTS + 1 steps with distinct inputs: every input slot and every engine's outputs are
+    reused; each step's result host buffer is reused too (read back before the next reuse).  In
+    "auto" mode the policy is forced to switch between the two track modes mid-stream."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2604_02586_b200.engine import FrameEngine, StreamingEngine
@@ -21,27 +31,63 @@ def test_streaming_matches_direct(zero_copy):
     target, valid = gd.tracks(d)
     g = np.ascontiguousarray(d["gaussians"])
     cams = d["cameras"]
+    n_steps = 2 * StreamingEngine.N_SLOTS + 1
+    shifts = [0.25 * ((k * 7) % 5) - 0.5 for k in range(n_steps)]
     inputs = []
-    for shift in (0.0, 0.75, -0.4, 0.0):
+    for shift in shifts:
         t = (target + np.array([shift, -0.5 * shift])).astype(np.float32)
         inputs.append((torch.from_numpy(g).pin_memory(), torch.from_numpy(t).pin_memory(),
                        torch.from_numpy(valid.astype(np.uint8)).pin_memory()))
-    streamer = StreamingEngine(zero_copy_tracks=zero_copy)
-    results = [StreamingEngine.result_buffer(len(g)) for _ in inputs]
-    events = [streamer.step(gh, cams, th, vh, res) for (gh, th, vh), res in zip(inputs, results)]
-    assert events[0] is None and all(e is not None for e in events[1:])
-    streamer.flush()
-    torch.cuda.synchronize()
+    base = FrameEngine()
+    streamer = StreamingEngine(base, zero_copy_tracks=zero_copy)
+    res_bufs = [StreamingEngine.result_buffer(len(g)) for _ in range(3)]  # reused round robin
+    got = [None] * n_steps
+    pending = []
+    if zero_copy == "auto":
+        # force mode switches mid-stream (the policy itself is unit-tested on the CPU suite):
+        # in place, copied, in place, ... with the device track buffers of "auto" in every slot
+        modes = iter([k % 4 < 2 for k in range(n_steps)])
+        streamer._choose_zero_copy = lambda *a: next(modes)
+    for k, (gh, th, vh) in enumerate(inputs):
+        ev = streamer.step(gh, cams, th, vh, res_bufs[k % 3])
+        if k == 0:
+            assert ev is None
+        else:
+            pending.append((k - 1, ev))
+        # read back the step whose buffer is about to be reused
+        while pending and pending[0][0] <= k - 2:
+            j, e = pending.pop(0)
+            e.synchronize()
+            got[j] = res_bufs[j % 3].clone()
+    ev = streamer.flush()
+    for j, e in pending:
+        e.synchronize()
+        got[j] = res_bufs[j % 3].clone()
+    ev.synchronize()
+    got[n_steps - 1] = res_bufs[(n_steps - 1) % 3].clone()
+    if zero_copy == "auto":
+        assert streamer.steps_zero_copy > 0 and streamer.steps_full_copy > 0
+    streamer.close()
+    assert base.plan.k2_ctas_per_sm == 0  # the passed-in engine's residency cap is restored
     direct = FrameEngine()
-    for (gh, th, vh), res in zip(inputs, results):
-        direct.bin(gh.numpy(), cams)
-        o = direct.compensate(th.numpy(), vh.numpy())
-        ref = torch.cat([o.delta_mean, o.rotation, o.scale,
-                         o.status.to(torch.float64)[:, None]], 1).cpu()
-        torch.testing.assert_close(res, ref, rtol=0, atol=0)
-    # the shifted inputs really produce different results
-    assert not torch.equal(results[0], results[1])
-    assert torch.equal(results[0], results[3])
+    for k, (gh, th, vh) in enumerate(inputs):
+        ref = _direct_rows(direct, gh.numpy(), cams, th.numpy(), vh.numpy())
+        torch.testing.assert_close(got[k], ref, rtol=0, atol=0, msg=f"step {k}")
+    assert not torch.equal(got[0], got[1])
+
+
+def test_compensate_rejects_mismatched_outputs():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_02586_b200.engine import FrameEngine
+    small = gd.load("scene21")
+    big = gd.load("scene7")
+    e_small = FrameEngine().bin(small["gaussians"], small["cameras"])
+    out = e_small.alloc_outputs()
+    t, v = gd.tracks(big)
+    e_big = FrameEngine().bin(big["gaussians"], big["cameras"])
+    with pytest.raises(ValueError):
+        e_big.compensate(t.astype(np.float32), v.astype(np.uint8), out)
 
 
 def test_trkf_batch_to_device(tmp_path):

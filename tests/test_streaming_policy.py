@@ -1,6 +1,7 @@
 """StreamingEngine's "auto" track policy (engine.py): copy the whole track arrays when that copy
-fits under the measured step period, read the occupied tiles in place otherwise, with hysteresis.
-Host logic only (fake CUDA events), so it runs on the CPU suite."""
+fits under the step period measured while reading in place, read the occupied tiles in place
+otherwise; hysteresis plus SWITCH_VOTES consecutive confirmations.  Host logic only (fake CUDA
+events), so it runs on the CPU suite."""
 
 import pytest
 
@@ -31,14 +32,19 @@ class _Arr:
         return 1
 
 
-def _engine(period_ms, steps=8):
+def _engine(period_ms, steps=8, in_place=True):
     se = StreamingEngine.__new__(StreamingEngine)  # no CUDA streams needed for the policy
     se.zero_copy_tracks = "auto"
     se._compute_ms = None
     se._periods = []
     se._last_zero_copy = True
-    se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms), 0) for k in range(steps)]
+    se._votes = 0
+    se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms), 0, in_place) for k in range(steps)]
     return se
+
+
+def _choose_n(se, mbytes, n):
+    return [_choose(se, mbytes) for _ in range(n)]
 
 
 def _choose(se, mbytes):
@@ -54,16 +60,39 @@ def test_auto_reads_in_place_when_the_copy_does_not_fit():
 
 def test_auto_copies_when_the_copy_hides_under_the_compute():
     se = _engine(period_ms=14.9)
-    assert _choose(se, 562.0) is False         # 11.2 ms < 0.85 * 14.9 ms
+    # 11.2 ms < 0.85 * 14.9 ms: switches after SWITCH_VOTES consecutive confirmations
+    votes = StreamingEngine.SWITCH_VOTES
+    assert _choose_n(se, 562.0, votes) == [True] * (votes - 1) + [False]
+    assert _choose(se, 562.0) is False
+
+
+def test_full_copy_periods_never_feed_the_estimate():
+    """Periods measured while copying contain the copy itself; they must not make the copy look
+    affordable (the self-reinforcing case of the round-1 driver run)."""
+    se = _engine(period_ms=4.0, steps=8, in_place=True)
+    _choose(se, 100.0)
+    assert se._compute_ms == pytest.approx(4.0)
+    se._timing = [(_Ev(100.0 + 9.0 * k), _Ev(100.0 + 9.0 * k), 0, False) for k in range(8)]
+    _choose(se, 100.0)
+    assert se._compute_ms == pytest.approx(4.0)
+
+
+def test_single_outlier_does_not_switch():
+    se = _engine(period_ms=4.4)
+    assert _choose(se, 273.0) is True
+    se._compute_ms, se._periods = 9.0, [9.0] * 5   # one step's estimate says "copy" ...
+    assert _choose(se, 273.0) is True
+    se._compute_ms, se._periods = 4.4, [4.4] * 5   # ... and the next says "in place" again
+    assert _choose_n(se, 273.0, 5) == [True] * 5
 
 
 def test_auto_hysteresis():
     se = _engine(period_ms=5.0)
     # in place: 4.4 ms copy is not below 0.85 * 5.0 = 4.25 ms -> stay in place
-    assert _choose(se, 220.0) is True
+    assert _choose_n(se, 220.0, 5) == [True] * 5
     se._last_zero_copy = False
     # copying: 4.4 ms is not above 0.95 * 5.0 = 4.75 ms -> keep copying
-    assert _choose(se, 220.0) is False
+    assert _choose_n(se, 220.0, 5) == [False] * 5
 
 
 def test_fixed_modes_ignore_the_period():
@@ -77,14 +106,14 @@ def test_fixed_modes_ignore_the_period():
 def test_periods_across_a_flush_are_ignored():
     se = _engine(period_ms=4.0, steps=4)
     # a burst boundary (flush) followed by a long idle gap: not a period
-    se._timing += [(_Ev(1000.0 + 4.0 * k), _Ev(1000.0 + 4.0 * k), 1) for k in range(4)]
+    se._timing += [(_Ev(1000.0 + 4.0 * k), _Ev(1000.0 + 4.0 * k), 1, True) for k in range(4)]
     _choose(se, 100.0)
     assert se._compute_ms == pytest.approx(4.0)
 
 
 def test_period_estimate_is_robust_to_a_slow_first_step():
     se = _engine(period_ms=4.0, steps=2)
-    se._timing = [(_Ev(0.0), _Ev(0.0), 0), (_Ev(30.0), _Ev(30.0), 0)] + \
-        [(_Ev(30.0 + 4.0 * k), _Ev(30.0 + 4.0 * k), 0) for k in range(1, 8)]
+    se._timing = [(_Ev(0.0), _Ev(0.0), 0, True), (_Ev(30.0), _Ev(30.0), 0, True)] + \
+        [(_Ev(30.0 + 4.0 * k), _Ev(30.0 + 4.0 * k), 0, True) for k in range(1, 12)]
     _choose(se, 100.0)
     assert se._compute_ms == pytest.approx(4.0)
