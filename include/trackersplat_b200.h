@@ -111,8 +111,12 @@ int ts_project(const double *gaussians, int64_t n, const ts_camera *camera, doub
  *      and :79-86; the regularisation tail is ts_regularize below).  Binning is per clip (it depends only on frame-1 Gaussians and cameras,
  *      as the weight maps in pipeline.py:191-196); accumulate/solve/fuse runs per target frame. */
 
-/* K1 projection + depth order + tile binning of N Gaussians into V views (all views must share
- * width/height).  Synchronises once (instance count).  Keeps the result in the plan. */
+/* K1 projection + depth order + tile binning of N Gaussians into V <= 64 views that share one
+ * width/height (TS_E_DIMENSION_MISMATCH otherwise).  Synchronises once (instance count).  Keeps
+ * the result in the plan.  Rigs with mixed image sizes or more views (the reference rasterizes
+ * each view at its own size, pipeline.py:117-120) are binned as same-size groups of <= 64 views,
+ * one plan each: ts_frame_compensate with updates == NULL per plan, then ts_update_all over all
+ * views (engine.FrameEngine does this). */
 int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_camera *cameras,
                  int32_t n_views, const ts_config *config, void *stream);
 
@@ -122,7 +126,8 @@ int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_cam
  * host arrays in place over PCIe (zero-copy), only the 8x8 quadrants of occupied tiles -- about
  * a tenth of the pixels at the benchmark configs; the host must not modify them until the
  * frame's work on `stream` completes.  Pageable host memory: TS_E_INVALID_ARGUMENT.
- * motions may have NULL members (then only the internal copy is kept); updates must be valid. */
+ * motions may have NULL members (then only the internal copy is kept).  updates == NULL stops
+ * after K3 (the per-view motions of a view group; motions must then be non-NULL). */
 int ts_frame_compensate(ts_plan *plan, const void *track_target, int32_t track_dtype,
                         const uint8_t *track_valid, const ts_motions *motions,
                         const ts_updates *updates, void *stream);

@@ -527,7 +527,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                         const uint8_t *track_valid, const ts_motions *motions,
                         const ts_updates *updates, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (!p || !updates || p->V < 1) return TS_E_INVALID_ARGUMENT;
+  if (!p || p->V < 1) return TS_E_INVALID_ARGUMENT;
+  if (!updates && !motions) return TS_E_INVALID_ARGUMENT;  // nothing would be returned
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
   const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
   // tracks: device memory, or pinned host memory that K2 reads in place (zero-copy: only the
@@ -583,6 +584,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 
+  if (!updates) return TS_OK;  // K2 + K3 only: the caller fuses (ts_update_all) over more views
   ENSURE(p->k4_ws, k4_workspace_bytes(n));
   cudaEvent_t e5 = p->mark_begin(s);
   launch_k4_fuse(p->gaussians, n, ptr<ts_camera>(p->cams), p->V, m, p->cfg, *updates,

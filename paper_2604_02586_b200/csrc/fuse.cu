@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
   for (int v = 0; v < V; v++) {
     const int64_t gv = (int64_t)v * n + g;
     if (m.status[gv] != TS_STATUS_SOLVED) continue;
-    mask |= 1ull << v;
+    if (v < 64) mask |= 1ull << v;
     n_solved++;
     tw += m.weight_sum[gv];
     tp += m.pixel_count[gv];
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
                   tp >= cfg.min_total_pixels;
   key[g] = ok ? (uint32_t)n_solved : 0u;  // descending sort: heaviest first, ineligible last
   val[g] = (uint32_t)g;
-  solved_mask[g] = ok ? mask : 0ull;
+  solved_mask[g] = ok ? (V <= 64 ? mask : ~0ull) : 0ull;  // > 64 views: bits rebuilt by k4_fuse
   if (!ok) {
     double delta[3] = {0.0, 0.0, 0.0}, q[4], sc[3];
 #pragma unroll

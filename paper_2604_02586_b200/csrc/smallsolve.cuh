@@ -590,7 +590,9 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   }
 #pragma unroll
   for (int i = 0; i < 4; i++) q[i] = gs[3 + i];
-  uint64_t solved = eligible_mask;  // bit v: view v SOLVED (V <= 64)
+  // bit v: view v SOLVED.  With more than 64 views the bits are rebuilt per 64-view word below
+  // and a nonzero eligible_mask only says "eligible".
+  uint64_t solved = eligible_mask;
   if (!solved) {
     int n_solved = 0;
     double tw = 0.0;
@@ -598,7 +600,7 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     for (int v = 0; v < V; v++) {
       const int64_t gv = (int64_t)v * n + g;
       if (m.status[gv] != TS_STATUS_SOLVED) continue;
-      solved |= 1ull << v;
+      if (v < 64) solved |= 1ull << v;
       n_solved++;
       tw += m.weight_sum[gv];
       tp += m.pixel_count[gv];
@@ -610,8 +612,15 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
   bool bad = false;
   // iterate the solved views only, in view order: Gaussians with equal solved-view counts (k4_fuse
   // groups them) then run the heavy body in lockstep
-  while (solved && !bad) {
-    const int v = ffs64_hd(solved) - 1;
+  for (int base = 0; base < V && !bad; base += 64) {
+   if (V > 64) {
+    solved = 0;
+    const int top = V - base < 64 ? V - base : 64;
+    for (int j = 0; j < top; j++)
+      if (m.status[(int64_t)(base + j) * n + g] == TS_STATUS_SOLVED) solved |= 1ull << j;
+   }
+   while (solved && !bad) {
+    const int v = base + ffs64_hd(solved) - 1;
     solved &= solved - 1;
     const int64_t gv = (int64_t)v * n + g;
     const ts_camera &cam = cams[v];
@@ -672,6 +681,7 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     qr_add_row_rhs<6>(R6, c6, L0, mc00);
     qr_add_row_rhs<6>(R6, c6, L1, mc01);
     qr_add_row_rhs<6>(R6, c6, L2, mc11);
+   }
   }
   if (bad) return TS_STATUS_UNSOLVABLE;
   return fuse_finish(gs, R4, R6, c6, cfg, delta, q, sc, allow_slow, dbg);

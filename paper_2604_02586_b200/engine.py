@@ -76,8 +76,29 @@ class FrameOutputs:
                 "unsolvable": int((st == 0).sum())}
 
 
+MAX_VIEWS_PER_PLAN = 64  # view bits of K1's 32-bit depth key (api.cu frame_bin)
+
+
+def view_groups(cam_rows, max_views=MAX_VIEWS_PER_PLAN):
+    """Consecutive runs of views with the same image size, at most `max_views` each: the unit one
+    binning plan handles (K1-K3); K4 then fuses every view at once."""
+    groups, v0 = [], 0
+    for v in range(1, len(cam_rows) + 1):
+        if (v == len(cam_rows) or v - v0 == max_views or
+                tuple(cam_rows[v][16:18]) != tuple(cam_rows[v0][16:18])):
+            groups.append((v0, v))
+            v0 = v
+    return groups
+
+
 class FrameEngine:
-    """Holds the per-clip binning and per-frame workspace of one device."""
+    """Holds the per-clip binning and per-frame workspace of one device.
+
+    The reference rasterizes every view at its own size (pipeline.py:117-120) and accepts any
+    number of views.  One binning plan covers up to 64 views of one image size; other camera
+    rigs are binned as consecutive same-size groups of <= 64 views, each with its own plan for
+    K1-K3, and K4 fuses all views at once (ts_update_all).  Tracks of such rigs are passed as
+    per-view lists."""
 
     def __init__(self, plan: nat.Plan | None = None):
         self.plan = plan if plan is not None else nat.Plan()
@@ -87,6 +108,12 @@ class FrameEngine:
         self.width = self.height = 0
         self._gauss = None
         self._cams = None
+        self._groups = None  # [(v0, v1, Plan)] when the views need more than one plan
+        self._sizes = []
+
+    @property
+    def grouped(self):
+        return self._groups is not None
 
     # -- K1 ------------------------------------------------------------------------------
     def bin(self, gaussians, cameras, config=None, stream=None):
@@ -100,14 +127,36 @@ class FrameEngine:
         self.n = int(self._gauss.shape[0])
         self.n_views = len(cam_rows)
         self.width, self.height = int(cam_rows[0][16]), int(cam_rows[0][17])
-        nat.check(self._lib.ts_frame_bin(self.plan.handle, nat.dptr(self._gauss), self.n,
-                                         self._cams, self.n_views, ctypes.byref(self._cfg),
-                                         nat.stream_ptr(stream)), "ts_frame_bin")
+        self._sizes = [(int(r[16]), int(r[17])) for r in cam_rows]
+        groups = view_groups(cam_rows)
+        if len(groups) == 1:
+            self._groups = None
+            nat.check(self._lib.ts_frame_bin(self.plan.handle, nat.dptr(self._gauss), self.n,
+                                             self._cams, self.n_views, ctypes.byref(self._cfg),
+                                             nat.stream_ptr(stream)), "ts_frame_bin")
+            return self
+        old = {(v0, v1): p for v0, v1, p in (self._groups or [])}
+        self._groups = []
+        for k, (v0, v1) in enumerate(groups):
+            plan = self.plan if k == 0 else old.get((v0, v1)) or nat.Plan()
+            sub = nat.make_cameras(cam_rows[v0:v1])
+            nat.check(self._lib.ts_frame_bin(plan.handle, nat.dptr(self._gauss), self.n, sub,
+                                             v1 - v0, ctypes.byref(self._cfg),
+                                             nat.stream_ptr(stream)), "ts_frame_bin")
+            self._groups.append((v0, v1, plan))
         return self
+
+    def _group_of(self, view):
+        for v0, v1, plan in self._groups:
+            if v0 <= view < v1:
+                return v0, plan
+        raise IndexError(view)
 
     def binning(self):
         """Copies of the binning arrays (tile keys, instance order, ranges, bbox, status)."""
         torch = _torch()
+        if self.grouped:
+            raise NotImplementedError("binning() of a grouped (multi-plan) camera rig")
         b = nat.Binning()
         nat.check(self._lib.ts_frame_binning(self.plan.handle, ctypes.byref(b)), "binning")
         torch.cuda.synchronize()
@@ -130,10 +179,13 @@ class FrameEngine:
 
     def occupied_tiles(self):
         """Non-empty (view, tile) lists of the current binning (K2 reads 256 track pixels each)."""
-        c = ctypes.c_int64(0)
-        nat.check(self._lib.ts_frame_occupied_tiles(self.plan.handle, ctypes.byref(c)),
-                  "occupied_tiles")
-        return int(c.value)
+        total = 0
+        for plan in ([self.plan] if not self.grouped else [g[2] for g in self._groups]):
+            c = ctypes.c_int64(0)
+            nat.check(self._lib.ts_frame_occupied_tiles(plan.handle, ctypes.byref(c)),
+                      "occupied_tiles")
+            total += int(c.value)
+        return total
 
     # -- K2 + K3 + K4 ----------------------------------------------------------------------
     def alloc_outputs(self):
@@ -173,10 +225,16 @@ class FrameEngine:
 
     def compensate(self, track_target, track_valid, out: FrameOutputs | None = None,
                    stream=None) -> FrameOutputs:
-        """Fused raster-accumulate, per-view affine fit and multi-view fuse for one frame."""
+        """Fused raster-accumulate, per-view affine fit and multi-view fuse for one frame.
+
+        Tracks: (V, H, W, 2) targets and (V, H, W) validity (device tensors, pinned host tensors
+        read in place by K2, or host arrays that are copied), or per-view lists of them (required
+        when the views differ in size)."""
         torch = _torch()
         if self._gauss is None:
             raise RuntimeError("FrameEngine.bin() must run before compensate()")
+        if self.grouped or isinstance(track_target, (list, tuple)):
+            return self._compensate_groups(track_target, track_valid, out, stream)
         tgt, val = track_target, track_valid
         # each array: a CUDA tensor as is; a pinned CPU tensor is read in place by K2 (zero-copy:
         # only the occupied tiles' quadrants cross PCIe); anything else is copied to the device
@@ -216,12 +274,83 @@ class FrameEngine:
                                                 nat.stream_ptr(stream)), "ts_frame_compensate")
         return out
 
+    def _track_pair(self, tgt, val):
+        """One (..., 2) target / validity pair as the C ABI takes it: device or pinned host."""
+        torch = _torch()
+        if _pinned(tgt):
+            if tgt.dtype not in (torch.float32, torch.float64):
+                raise TypeError("pinned track targets must be float32 or float64")
+        elif not isinstance(tgt, torch.Tensor):
+            tgt = np.asarray(tgt)
+            tgt = as_device(tgt, torch.float32 if tgt.dtype == np.float32 else torch.float64)
+        else:
+            tgt = tgt.contiguous()
+            if tgt.device.type != "cuda":
+                tgt = as_device(tgt, tgt.dtype)
+        if _pinned(val):
+            if val.dtype != torch.uint8:
+                raise TypeError("pinned track validity must be uint8")
+        else:
+            val = as_device(val, torch.uint8)
+        return tgt, val
+
+    def _compensate_groups(self, targets, valids, out, stream):
+        """Per-view track lists, and rigs binned as several plans: K2+K3 per plan into the
+        plan's slice of the view-major motion arrays, then K4 over every view."""
+        torch = _torch()
+        from .errors import DimensionMismatch
+        if len(targets) != self.n_views or len(valids) != self.n_views:
+            raise DimensionMismatch("track fields and cameras count differ")
+        tv = []
+        for v in range(self.n_views):
+            tgt, val = self._track_pair(targets[v], valids[v])
+            w, h = self._sizes[v]
+            if tuple(tgt.shape) != (h, w, 2) or tuple(val.shape) != (h, w):
+                raise DimensionMismatch(f"view {v}: tracks {tuple(tgt.shape)} / "
+                                        f"{tuple(val.shape)} vs camera {w}x{h}")
+            tv.append((tgt, val))
+        if out is None:
+            out = self.alloc_outputs()
+        else:
+            self.check_outputs(out)
+        groups = self._groups or [(0, self.n_views, self.plan)]
+        n = self.n
+        for v0, v1, plan in groups:
+            dt = torch.float64 if any(t.dtype == torch.float64 for t, _ in tv[v0:v1]) \
+                else torch.float32
+            tgt = torch.stack([t.to("cuda", dt) for t, _ in tv[v0:v1]])
+            val = torch.stack([x.to("cuda") for _, x in tv[v0:v1]])
+            off = v0 * n
+
+            def at(t, k=1):
+                return nat.dptr(t).value + off * k * t.element_size()
+            m = nat.Motions(at(out.motion_status), at(out.motion_a, 4), at(out.motion_b, 2),
+                            at(out.weight_sum), at(out.pixel_count), at(out.static_pixel_count),
+                            at(out.static_weight_sum))
+            nat.check(self._lib.ts_frame_compensate(
+                plan.handle, nat.dptr(tgt),
+                nat.TS_TRACK_F32 if dt == torch.float32 else nat.TS_TRACK_F64, nat.dptr(val),
+                ctypes.byref(m), None, nat.stream_ptr(stream)), "ts_frame_compensate")
+        m = nat.Motions(nat.dptr(out.motion_status).value, nat.dptr(out.motion_a).value,
+                        nat.dptr(out.motion_b).value, nat.dptr(out.weight_sum).value,
+                        nat.dptr(out.pixel_count).value, nat.dptr(out.static_pixel_count).value,
+                        nat.dptr(out.static_weight_sum).value)
+        u = nat.Updates(nat.dptr(out.delta_mean).value, nat.dptr(out.rotation).value,
+                        nat.dptr(out.scale).value, nat.dptr(out.status).value)
+        nat.check(self._lib.ts_update_all(nat.dptr(self._gauss), n, self._cams, self.n_views,
+                                          ctypes.byref(m), ctypes.byref(self._cfg),
+                                          ctypes.byref(u), nat.stream_ptr(stream)),
+                  "ts_update_all")
+        return out
+
     def dominant_gaussians(self, view, stream=None):
         """Per-pixel dominant Gaussian id (-1 if none) and its depth (scene.py:166-189)."""
         torch = _torch()
-        gid = torch.empty((self.height, self.width), dtype=torch.int64, device="cuda")
-        dep = torch.empty((self.height, self.width), dtype=torch.float64, device="cuda")
-        nat.check(self._lib.ts_dominant_gaussians(self.plan.handle, int(view), nat.dptr(gid),
+        w, h = self._sizes[view]
+        gid = torch.empty((h, w), dtype=torch.int64, device="cuda")
+        dep = torch.empty((h, w), dtype=torch.float64, device="cuda")
+        v0, plan = self._group_of(view) if self.grouped else (0, self.plan)
+        nat.check(self._lib.ts_dominant_gaussians(plan.handle, int(view - v0), nat.dptr(gid),
                                                   nat.dptr(dep), nat.stream_ptr(stream)),
                   "ts_dominant_gaussians")
         return gid, dep

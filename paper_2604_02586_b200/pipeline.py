@@ -100,6 +100,17 @@ def _tracks_arrays(tracks, n_views):
         return tracks
     if len(tracks) != n_views:
         raise DimensionMismatch("track fields and cameras count differ")
+    if len({(t.width, t.height) for t in tracks}) > 1:
+        # per-view image sizes (pipeline.py:117-120): per-view lists, FrameEngine bins size groups
+        tgts, vals = [], []
+        for t in tracks:
+            tg = np.asarray(t.target)
+            va = np.asarray(t.valid, bool)
+            if np.all(tg[va] == tg[va].astype(np.float32)):
+                tg = tg.astype(np.float32)
+            tgts.append(tg)
+            vals.append(va.astype(np.uint8))
+        return tgts, vals
     target = np.stack([np.asarray(t.target) for t in tracks])
     valid = np.stack([np.asarray(t.valid, bool) for t in tracks]).astype(np.uint8)
     if np.all(target[valid.astype(bool)] == target[valid.astype(bool)].astype(np.float32)):
