@@ -60,7 +60,8 @@ struct ts_plan {
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf k2_stats;
-  DevBuf partial, flag, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt, mot_sw;
+  DevBuf partial, flag, touched, k3_list, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
+      mot_sw;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
@@ -121,7 +122,8 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->acc_order, &p->acc_iota, &p->seg_start, &p->seg_end,
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
-                          &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched};
+                          &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
+                          &p->touched, &p->k3_list};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -138,7 +140,8 @@ void release_all(ts_plan *p) {
                     &p->acc_keys, &p->acc_keys2, &p->acc_order, &p->acc_iota, &p->seg_start,
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
-                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched};
+                    &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
+                    &p->touched, &p->k3_list};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -564,15 +567,22 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
+  const bool use_touched = k2_writes_touched();
+  if (use_touched) {
+    ENSURE(p->touched, NV + 8);
+    ENSURE(p->k3_list, 4 * (NV + 8));
+  }
   cudaEvent_t e3 = p->mark_begin(s);
   TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
+  if (use_touched) TS_CUDA_TRY(cudaMemsetAsync(p->touched.p, 0, NV + 8, s));
   TS_CUDA_TRY(launch_k2(K2_ACCUMULATE, track_dtype, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
                         ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
                         ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0, p->tpv * p->V,
                         track_target, track_valid, p->W, p->H, p->tiles_x, p->tpv, p->cfg,
                         ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0, nullptr,
                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, k2_stats(p, s),
-                        p->k2_sched.p, s, p->k2_ctas_per_sm));
+                        p->k2_sched.p, s, p->k2_ctas_per_sm,
+                        use_touched ? ptr<uint8_t>(p->touched) : nullptr));
   k2_stats_report(p, s);
   p->mark_end(ST_RASTER, e3, s);
 
@@ -580,7 +590,10 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   // fits inside a 200-register thread and measured 3.0 ms vs 0.6 + 1.5 ms (cfg2).
   cudaEvent_t e4 = p->mark_begin(s);
   launch_k3_solve(ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), ptr<uint32_t>(p->inst_base),
-                  ptr<uint32_t>(p->ntiles), ptr<int16_t>(p->bbox), NV, p->cfg, m, s);
+                  ptr<uint32_t>(p->ntiles), ptr<int16_t>(p->bbox), NV, p->cfg, m,
+                  use_touched ? ptr<uint8_t>(p->touched) : nullptr,
+                  use_touched ? ptr<uint32_t>(p->k3_list) : nullptr,
+                  use_touched ? ptr<uint32_t>(p->k3_list) + NV + 4 : nullptr, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 
@@ -779,20 +792,6 @@ int ts_update_all(const double *gaussians, int64_t n, const ts_camera *cameras, 
   cudaFreeAsync(dcams, s);
   cudaFreeAsync(ws, s);
   return e == cudaSuccess ? TS_OK : TS_E_CUDA;
-}
-
-int ts_debug_fuse_one(const double *gaussians, int64_t n, const ts_camera *cameras,
-                      int32_t n_views, const ts_motions *motions, const ts_config *config,
-                      int64_t g, double *dbg, void *stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  void *dcams = nullptr;
-  TS_CUDA_TRY(cudaMallocAsync(&dcams, sizeof(ts_camera) * n_views, s));
-  TS_CUDA_TRY(cudaMemcpyAsync(dcams, cameras, sizeof(ts_camera) * n_views, cudaMemcpyHostToDevice, s));
-  launch_k4_debug(gaussians, n, reinterpret_cast<ts_camera *>(dcams), n_views, *motions, *config, g,
-                  dbg, s);
-  cudaFreeAsync(dcams, s);
-  TS_CUDA_TRY(cudaGetLastError());
-  return TS_OK;
 }
 
 int ts_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch, int32_t max_rows,

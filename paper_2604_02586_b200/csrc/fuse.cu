@@ -236,21 +236,8 @@ __global__ void k_decompose_batch(const double *__restrict__ sigma, const double
 }
 
 // debug: intermediates of one Gaussian (E, ev, ref quat, covariance solution)
-__global__ void k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                         ts_config cfg, int64_t g, double *dbg) {
-  double gs[11];
-  for (int k = 0; k < 11; k++) gs[k] = G[11 * g + k];
-  double delta[3], q[4], sc[3];
-  fuse_gaussian(gs, g, n, cams, V, m, cfg, delta, q, sc, dbg);
-  for (int i = 0; i < 4; i++) dbg[22 + i] = q[i];
-}
-
 static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                     const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s) {
-  k4_debug<<<1, 1, 0, s>>>(G, n, cams, V, m, cfg, g, dbg);
-}
 // workspace: [counter | deferred records | 4 key/value arrays | CUB temp]
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 static size_t k4_sort_temp_bytes(int64_t n) {

@@ -27,13 +27,16 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm = 0);
+                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm = 0,
+                      uint8_t *touched = nullptr);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
+bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched bytes
 
 // K3: per-(view, Gaussian) affine fit from the tile partials of K2.
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
-                     const ts_config &cfg, ts_motions m, cudaStream_t s);
+                     const ts_config &cfg, ts_motions m, const uint8_t *touched, uint32_t *list,
+                     uint32_t *n_list, cudaStream_t s);
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
                       int64_t n, double det_floor, int min_pixels, double min_weight,
@@ -51,8 +54,6 @@ void launch_accumulate(int64_t n, const uint32_t *seg_start, const uint32_t *seg
 size_t k4_workspace_bytes(int64_t n);
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
                     const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s);
-void launch_k4_debug(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                     const ts_config &cfg, int64_t g, double *dbg, cudaStream_t s);
 void launch_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch,
                               int max_rows, double *x, int8_t *status, cudaStream_t s);
 void launch_cov3d_batch(const double *lin, const double *rhs, const int32_t *n_rows,

@@ -56,6 +56,7 @@ struct K2Params {
   // accumulate mode
   Partial *partial;  // one slot per (gv, 8x8 quadrant of its bbox)
   uint8_t *flag;
+  uint8_t *touched;  // per gv: 1 once it has a tracked contribution (k2_accum), zeroed before
   // emit mode
   unsigned long long *emit_count;
   int64_t emit_cap;
@@ -85,7 +86,7 @@ template <typename TrackT>
 struct K2Warp {
   RasterRec rec[32];
   uint64_t rect[32];  // bbox of the record clipped to the quadrant, as a 64-pixel bit mask
-  uint32_t slot[32];
+  uint32_t slot[32], gvid[32];
   int2 anc[32];       // moment anchor (bbox centre pixel) of each record (accumulate mode)
   double w[K2_FLUSH][K2_WROW];
   TrackT trk_u[64], trk_v[64];  // track targets in their input precision
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         if (hit) {
           S.rec[lane] = r;
           S.rect[lane] = rect;
+          S.gvid[lane] = gv;
           if (MODE == K2_ACCUMULATE) {
             // one slot per 8x8 quadrant of the gv's bbox, row-major from its top-left quadrant
             const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
               if (!__any_sync(0xffffffffu, c0 || c1)) st[K2S_EVAL_EMPTY]++;
             }
             if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
+              if (lane == 0 && P.touched) P.touched[S.gvid[j]] = 1;
               if (k0) S.w[kpend][lane] = w0;
               if (k1) S.w[kpend][lane + 32] = w1;
               if ((lane & (K2_FLUSH - 1)) == kpend) {  // this Gaussian's flush lanes
@@ -427,18 +430,20 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
 //
 // Same work units, culling and arithmetic as k2_raster, but the culled Gaussians of a unit are
 // appended (in depth order) to a per-warp batch of K2B_BATCH entries in shared memory (SoA), and a
-// full batch is processed pixel-parallel: each lane holds, for each of its two pixels, the bit mask
-// of batch entries whose bbox covers it, and walks those entries front to back.  Two candidates
-// per lane per trip (from either pixel's list) have their alphas evaluated independently -- alpha
-// does not depend on T -- and are then composited in order into the pixel's T.  A warp trip thus
-// evaluates up to 64 (Gaussian, pixel) pairs instead of one Gaussian's 64 pixel slots, so the
-// fp64 lanes are busy with candidates rather than bbox padding.  The moments of the batch's
-// entries are then reduced by two lanes per entry (alternate contributing pixels, one xor
-// shuffle), each entry's (gv, quadrant) slot written once.  Arithmetic per pair is the same as
-// k2_raster (q in numpy's order, table exp, T as the running product), so the contribution set,
-// alpha, T and the integer counts are bit-identical to it; only the summation order of the
-// moments differs.
-constexpr int K2B_BATCH = 16;   // entries per batch (two flush lanes each)
+// full batch is processed in three warp-wide phases instead of one Gaussian at a time:
+//   1. alpha: the batch's candidate (entry, pixel) pairs -- bbox x quadrant, unsaturated pixels --
+//      are listed in shared memory (row = entry x pixel half, in (entry, pixel) order) and
+//      evaluated 32 per round, one per lane: q, the keep predicate and alpha do not depend on
+//      T, so every lane evaluates a real candidate instead of one Gaussian's 64 pixel slots
+//      (the lane utilisation of the pixel-owned loop was 19.6/32);
+//   2. compositing: each lane walks its two pixels' candidate entries front to back with the
+//      alphas from phase 1 (w = alpha T, T *= 1 - alpha: a few instructions per step);
+//   3. moments: the lane pair of each entry walks the entry's two list rows and reduces its
+//      anchored moments (one xor shuffle), each entry's (gv, quadrant) slot written once.
+// Arithmetic per pair is k2_raster's (q in numpy's order, table exp, T as the running product),
+// so the contribution set, alpha, T and the integer counts are bit-identical to it; only the
+// summation order of the moments differs.
+constexpr int K2B_BATCH = 11;   // entries per batch (two list rows / flush lanes each)
 constexpr int K2B_WARPS = 4;
 
 template <typename TrackT>
@@ -446,124 +451,107 @@ struct K2BWarp {
   double mx[K2B_BATCH], my[K2B_BATCH], i00[K2B_BATCH], i01x2[K2B_BATCH], i11[K2B_BATCH],
       op[K2B_BATCH];
   uint64_t rect[K2B_BATCH];
-  uint32_t slot[K2B_BATCH];
+  uint32_t slot[K2B_BATCH], gv[K2B_BATCH];
   int ax[K2B_BATCH], ay[K2B_BATCH];
-  double w[K2B_BATCH][K2_WROW];
+  double w[K2B_BATCH][K2_WROW];           // alpha after phase 1, w = alpha T (or 0) after phase 2
+  uint16_t pair[K2B_BATCH * 64];          // candidate list: entry << 6 | pixel
   TrackT trk_u[64], trk_v[64];
 };
 
-// alpha of one batch entry at one pixel; pass = q <= 9 && alpha >= cutoff (splat.py:153-155)
-template <typename TrackT>
-__device__ __forceinline__ double k2b_alpha(const K2BWarp<TrackT> &S, int k, double fpx,
-                                            double fpy, double cutoff, const double *etab,
-                                            bool &pass) {
-  const double dx = sub(fpx, S.mx[k]), dy = sub(fpy, S.my[k]);
-  const double q = add(add(mul(mul(S.i00[k], dx), dx), mul(mul(S.i01x2[k], dx), dy)),
-                       mul(mul(S.i11[k], dy), dy));
-  const bool in = q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS;
-  const double a = alpha_of_table(S.op[k], in ? q : 0.0, etab);  // table index stays in range
-  pass = in && a >= cutoff;
-  return a;
-}
-
 template <typename TrackT>
 __device__ __forceinline__ void k2b_process(K2BWarp<TrackT> &S, const K2Params &P, int lane,
-                                            int nb, double fpx, double fpy0, double fpy1,
-                                            bool valid0, bool valid1, double &T0, double &T1,
-                                            uint64_t &done64, uint64_t static64, int qx0,
-                                            int qy0, const double *etab) {
+                                            int nb, bool valid0, bool valid1, double &T0,
+                                            double &T1, uint64_t &done64, uint64_t static64,
+                                            int qx0, int qy0, const double *etab) {
   __syncwarp();
   const double es = P.early_stop, cutoff = P.alpha_cutoff;
-  // candidate entries of each of the lane's pixels (bit k = entry k, depth order)
-  uint32_t mA = 0, mB = 0;
-  for (int k = 0; k < nb; k++) {
-    const uint64_t r = S.rect[k];
-    mA |= (uint32_t)((r >> lane) & 1ull) << k;
-    mB |= (uint32_t)((r >> (lane + 32)) & 1ull) << k;
+  // ---- candidate list: lane r = list row (entry r >> 1, pixel half r & 1)
+  const int e = lane >> 1, h = lane & 1;
+  uint32_t row = 0;
+  if (e < nb) row = (uint32_t)((S.rect[e] & ~done64) >> (32 * h));
+  const int cnt_row = __popc(row);
+  int off = cnt_row;  // inclusive scan over the 32 rows
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += o;
   }
-  if (!(T0 >= es)) mA = 0;
-  if (!(T1 >= es)) mB = 0;
-  uint32_t cA = 0, cB = 0;  // entries with a tracked contribution at the pixel
+  const int total = __shfl_sync(0xffffffffu, off, 31);
+  off -= cnt_row;  // exclusive
+  {
+    uint32_t b = row;
+    int i = off;
+    const uint16_t hi = (uint16_t)((e << 6) | (32 * h));
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      S.pair[i++] = (uint16_t)(hi | bit);
+    }
+  }
+  __syncwarp();
+  // ---- phase 1: alpha of every candidate pair, one per lane per round (splat.py:153-155)
+  for (int i = lane; i < total; i += 32) {
+    const int pr = S.pair[i];
+    const int k = pr >> 6, p = pr & 63;
+    const double fpx = (double)(qx0 + (p & 7)), fpy = (double)(qy0 + (p >> 3));
+    const double dx = sub(fpx, S.mx[k]), dy = sub(fpy, S.my[k]);
+    const double q = add(add(mul(mul(S.i00[k], dx), dx), mul(mul(S.i01x2[k], dx), dy)),
+                         mul(mul(S.i11[k], dy), dy));
+    const bool in = q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS;
+    const double a = alpha_of_table(S.op[k], in ? q : 0.0, etab);  // table index in range
+    S.w[k][p] = (in && a >= cutoff) ? a : 0.0;  // alpha >= cutoff > 0: 0 marks "no keep"
+  }
+  // each pixel's candidate entries (bit k = entry k, depth order)
+  uint32_t mA = 0, mB = 0;
+  {
+    const uint32_t nd_lo = ~(uint32_t)done64, nd_hi = ~(uint32_t)(done64 >> 32);
+    for (int k = 0; k < nb; k++) {
+      const uint64_t r = S.rect[k];
+      mA |= (((uint32_t)r & nd_lo) >> lane & 1u) << k;
+      mB |= (((uint32_t)(r >> 32) & nd_hi) >> lane & 1u) << k;
+    }
+  }
+  __syncwarp();
+  // ---- phase 2: compositing front to back (splat.py:182-193, motion2d.py:151); every kept
+  // alpha lowers T, a pair contributes while T >= early_stop and its pixel has a valid track
   while (__any_sync(0xffffffffu, (mA | mB) != 0u)) {
-    // two candidates per trip: the next of pixel A and the next of pixel B; when one list is
-    // empty both come from the other (in order: alpha is independent of T)
-    int k1 = -1, k2 = -1;
-    bool b1 = false, b2 = false;
     if (mA) {
-      k1 = __ffs(mA) - 1;
+      const int k = __ffs(mA) - 1;
       mA &= mA - 1;
-    } else if (mB) {
-      k1 = __ffs(mB) - 1;
-      mB &= mB - 1;
-      b1 = true;
+      const double a = S.w[k][lane];
+      const bool keep = a > 0.0 && T0 >= es;
+      const double w = mul(a, T0);
+      if (a > 0.0) T0 = mul(T0, sub(1.0, a));
+      S.w[k][lane] = (keep && valid0) ? w : 0.0;
     }
     if (mB) {
-      k2 = __ffs(mB) - 1;
+      const int k = __ffs(mB) - 1;
       mB &= mB - 1;
-      b2 = true;
-    } else if (mA) {
-      k2 = __ffs(mA) - 1;
-      mA &= mA - 1;
+      const double a = S.w[k][lane + 32];
+      const bool keep = a > 0.0 && T1 >= es;
+      const double w = mul(a, T1);
+      if (a > 0.0) T1 = mul(T1, sub(1.0, a));
+      S.w[k][lane + 32] = (keep && valid1) ? w : 0.0;
     }
-    bool pass1 = false, pass2 = false;
-    double a1 = 0.0, a2 = 0.0;
-    if (k1 >= 0) a1 = k2b_alpha(S, k1, fpx, b1 ? fpy1 : fpy0, cutoff, etab, pass1);
-    if (k2 >= 0) a2 = k2b_alpha(S, k2, fpx, b2 ? fpy1 : fpy0, cutoff, etab, pass2);
-    // composite in depth order (k1 before k2 when both are the same pixel's)
-    if (pass1) {
-      const double tin = b1 ? T1 : T0;
-      if (tin >= es) {
-        const double tout = mul(tin, sub(1.0, a1));
-        if (b1) T1 = tout; else T0 = tout;
-        if (b1 ? valid1 : valid0) {
-          S.w[k1][b1 ? lane + 32 : lane] = mul(a1, tin);  // motion2d.py:151
-          if (b1) cB |= 1u << k1; else cA |= 1u << k1;
-        }
-      }
-    }
-    if (pass2) {
-      const double tin = b2 ? T1 : T0;
-      if (tin >= es) {
-        const double tout = mul(tin, sub(1.0, a2));
-        if (b2) T1 = tout; else T0 = tout;
-        if (b2 ? valid1 : valid0) {
-          S.w[k2][b2 ? lane + 32 : lane] = mul(a2, tin);
-          if (b2) cB |= 1u << k2; else cA |= 1u << k2;
-        }
-      }
-    }
-    if (!(T0 >= es)) mA = 0;  // saturated: the pixel's later entries are all cut
-    if (!(T1 >= es)) mB = 0;
   }
   done64 = (uint64_t)__ballot_sync(0xffffffffu, !(T0 >= es)) |
            ((uint64_t)__ballot_sync(0xffffffffu, !(T1 >= es)) << 32);
-  // per-entry contribution masks, kept by the entry's two flush lanes (lane & 15)
-  const int e = lane & (K2B_BATCH - 1), h = lane / K2B_BATCH;
-  uint64_t cm = 0;
-  for (int k = 0; k < nb; k++) {
-    const uint64_t mk = (uint64_t)__ballot_sync(0xffffffffu, (cA >> k) & 1u) |
-                        ((uint64_t)__ballot_sync(0xffffffffu, (cB >> k) & 1u) << 32);
-    if (e == k) cm = mk;
-  }
   __syncwarp();
-  // moments (motion2d.py:144-160) anchored at the entry's bbox centre pixel: lane h of entry e
-  // sums its (h-th, h+2-th, ...) contributing pixels, one xor shuffle adds the two halves
+  // ---- phase 3: moments (motion2d.py:144-160) anchored at the entry's bbox centre pixel; lane
+  // (e, h) sums the contributions of its list row, one xor shuffle adds the entry's two rows
   double m[TS_NMOM];
 #pragma unroll
   for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
   uint32_t cnt = 0, scnt = 0;
-  if (cm) {
+  if (cnt_row) {
     const int ax = S.ax[e], ay = S.ay[e];
     const double fax = (double)ax, fay = (double)ay;
-    const double bx = (double)(qx0 - ax), by = (double)(qy0 - ay);
-    uint64_t bits = cm;
-    if (h) bits &= bits - 1;
-    while (bits) {
-      const int p = __ffsll((long long)bits) - 1;
-      bits &= bits - 1;
-      bits &= bits - 1;
+    const uint32_t st32 = (uint32_t)(static64 >> (32 * h));
+    for (int i = off; i < off + cnt_row; i++) {
+      const int p = S.pair[i] & 63;
       const double w = S.w[e][p];
-      const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
+      if (w == 0.0) continue;  // w = alpha T >= cutoff * early_stop > 0 for a contribution
+      const double dx = (double)(qx0 + (p & 7) - ax), dy = (double)(qy0 + (p >> 3) - ay);
       const double ua = (double)S.trk_u[p] - fax, va = (double)S.trk_v[p] - fay;
       const double wx = w * dx, wy = w * dy;
       m[0] += w;
@@ -578,17 +566,17 @@ __device__ __forceinline__ void k2b_process(K2BWarp<TrackT> &S, const K2Params &
       m[9] += wx * va;
       m[10] += wy * ua;
       m[11] += wy * va;
-      const bool st = (static64 >> p) & 1ull;
+      const uint32_t st = (st32 >> (p & 31)) & 1u;
       m[12] += st ? w : 0.0;
       scnt += st;
       cnt++;
     }
   }
 #pragma unroll
-  for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], K2B_BATCH);
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, K2B_BATCH);
-  scnt += __shfl_xor_sync(0xffffffffu, scnt, K2B_BATCH);
-  if (cm && e < nb) {
+  for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], 1);
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+  scnt += __shfl_xor_sync(0xffffffffu, scnt, 1);
+  if (cnt && e < nb) {
     Partial *dst = P.partial + S.slot[e];
     if (h == 0) {
       dst->m[0] = m[0]; dst->m[1] = m[1]; dst->m[2] = m[2]; dst->m[3] = m[3];
@@ -599,13 +587,14 @@ __device__ __forceinline__ void k2b_process(K2BWarp<TrackT> &S, const K2Params &
       dst->count = cnt;
       dst->static_count = scnt;
       P.flag[S.slot[e]] = 1;
+      if (P.touched) P.touched[S.gv[e]] = 1;
     }
   }
   __syncwarp();
 }
 
 template <typename TrackT>
-__global__ void __launch_bounds__(K2B_WARPS * 32) k2_accum(const K2Params P) {
+__global__ void __launch_bounds__(K2B_WARPS * 32, 6) k2_accum(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
   double *etab = reinterpret_cast<double *>(k2_smem_raw);  // exp(-k/64), k = 0..288
   for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
@@ -669,9 +658,9 @@ __global__ void __launch_bounds__(K2B_WARPS * 32) k2_accum(const K2Params P) {
       bool hit = false;
       RasterRec r;
       uint64_t rect = 0;
-      uint32_t ibase = 0;
+      uint32_t ibase = 0, gv = 0;
       if (i < end) {
-        const uint32_t gv = P.inst_gv[i];
+        gv = P.inst_gv[i];
         ibase = __ldg(P.inst_base + gv);
         r = P.rec[gv];
         rect = quad_rect(r, qx0, qy0);
@@ -695,21 +684,20 @@ __global__ void __launch_bounds__(K2B_WARPS * 32) k2_accum(const K2Params P) {
           const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
           S.slot[k] = ibase + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
                                          ((qx0 >> 3) - bx0));
+          S.gv[k] = gv;
           S.ax[k] = anchor_x(r);
           S.ay[k] = anchor_y(r);
         }
         hm &= ~__ballot_sync(0xffffffffu, mine);
         nb += take;
         if (nb == K2B_BATCH) {
-          k2b_process(S, P, lane, nb, fpx, fpy0, fpy1, valid0, valid1, T0, T1, done64, static64,
-                      qx0, qy0, etab);
+          k2b_process(S, P, lane, nb, valid0, valid1, T0, T1, done64, static64, qx0, qy0, etab);
           nb = 0;
         }
       }
     }
     if (nb > 0)
-      k2b_process(S, P, lane, nb, fpx, fpy0, fpy1, valid0, valid1, T0, T1, done64, static64, qx0,
-                  qy0, etab);
+      k2b_process(S, P, lane, nb, valid0, valid1, T0, T1, done64, static64, qx0, qy0, etab);
   }
 }
 
@@ -778,6 +766,13 @@ static cudaError_t launch_mode(const K2Params &P, cudaStream_t s, int cap) {
   return cudaGetLastError();
 }
 
+bool k2_writes_touched() { return true; }  // both accumulate kernels mark touched gvs
+
+static bool k2_legacy() {
+  static const bool legacy = std::getenv("TS_K2_LEGACY") != nullptr;  // A/B of the two loops
+  return legacy;
+}
+
 template <typename TrackT>
 static cudaError_t launch_accum(const K2Params &P, cudaStream_t s, int cap) {
   auto kern = k2_accum<TrackT>;
@@ -802,7 +797,8 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       unsigned long long *emit_count, int64_t emit_cap, uint64_t *emit_key,
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
-                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm) {
+                      unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm,
+                      uint8_t *touched) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -842,6 +838,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.static_thr = cfg.static_threshold_px;
   P.partial = partial;
   P.flag = flag;
+  P.touched = touched;
   P.emit_count = emit_count;
   P.emit_cap = emit_cap;
   P.emit_key = emit_key;
@@ -853,8 +850,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.dom_depth = dom_depth;
   P.stats = stats;
   if (mode == K2_ACCUMULATE) {
-    static const bool legacy = std::getenv("TS_K2_LEGACY") != nullptr;  // A/B of the old loop
-    if (legacy) {
+    if (k2_legacy()) {
       if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
       return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
     }

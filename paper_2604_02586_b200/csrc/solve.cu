@@ -12,6 +12,8 @@
 // Stage accumulate_view (motion2d.py:126-161): contributions are stably sorted by Gaussian id and
 // one thread per Gaussian adds them in array order with the reference's exact products
 // ((w*h_i)*h_j, no FMA), so the result equals np.add.at bit-for-bit.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "motion.cuh"
@@ -93,6 +95,93 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial 
     if (lane == j)
       store_motion(m, gv, solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels,
                                         min_weight));
+  }
+}
+
+// K3 split by K2's per-gv "touched" bytes (a gv with at least one tracked contribution).  At the
+// large configs most gvs are occluded (cfg5: ~7% touched), and a warp with any touched lane
+// waited on the whole bbox -> slot base -> flags -> partials chain.  Instead:
+//   k3_defaults: every gv's motion = UNSOLVABLE / A = I / b = 0 / zero sums, coalesced streaming
+//                stores, and the touched gvs appended to a list (warp-aggregated atomic);
+//   k3_solve_list: the fit of the listed gvs (one thread each, big bboxes per warp as k3_solve),
+//                  overwriting their defaults (same stream, after k3_defaults).
+// The list order varies run to run; every gv's result does not depend on it.
+__global__ void __launch_bounds__(256) k3_defaults(const uint8_t *__restrict__ touched, int64_t NV,
+                                                   ts_motions m, uint32_t *__restrict__ list,
+                                                   uint32_t *__restrict__ n_list) {
+  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = gv < NV;
+  const bool t = valid && touched[gv] != 0;
+  if (valid) {
+    GvMotion r;
+    r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
+    r.b[0] = 0.0; r.b[1] = 0.0;
+    r.wsum = 0.0;
+    r.static_wsum = 0.0;
+    r.count = 0;
+    r.static_count = 0;
+    r.status = TS_STATUS_UNSOLVABLE;
+    store_motion(m, gv, r);
+  }
+  const uint32_t tm = __ballot_sync(0xffffffffu, t);
+  if (!tm) return;
+  uint32_t base = 0;
+  const int leader = __ffs(tm) - 1;
+  if (lane == leader) base = atomicAdd(n_list, (uint32_t)__popc(tm));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (t) list[base + __popc(tm & ((1u << lane) - 1u))] = (uint32_t)gv;
+}
+
+__global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
+    const Partial *__restrict__ partial, const uint8_t *__restrict__ flag,
+    const uint32_t *__restrict__ inst_base, const int16_t *__restrict__ bbox,
+    const uint32_t *__restrict__ list, const uint32_t *__restrict__ n_list, double det_floor,
+    int min_pixels, double min_weight, ts_motions m) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nl = *n_list;
+  // grid-stride over the device-side count (the grid is sized for the SMs, not the worst case)
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nl; base += gridDim.x * blockDim.x) {
+  const uint32_t i = base + threadIdx.x;
+  const bool valid = i < nl;
+  const int64_t gv = valid ? (int64_t)list[i] : 0;
+  const short4 bb = valid ? reinterpret_cast<const short4 *>(bbox)[gv] : make_short4(0, -1, 0, -1);
+  const uint32_t nq = (uint32_t)(((bb.y >> 3) - (bb.x >> 3) + 1) * ((bb.w >> 3) - (bb.z >> 3) + 1));
+  const bool big = nq > K3_BIG;
+  uint32_t sb = 0;
+  int ax = 0, ay = 0;
+  if (nq) {
+    sb = inst_base[gv];
+    ax = ((int)bb.x + (int)bb.y) >> 1;
+    ay = ((int)bb.z + (int)bb.w) >> 1;
+  }
+  if (valid && !big) {
+    const GvMotion r = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels,
+                                min_weight);
+    store_motion(m, gv, r);
+  }
+  uint32_t bigmask = __ballot_sync(0xffffffffu, valid && big);
+  while (bigmask) {
+    const int j = __ffs(bigmask) - 1;
+    bigmask &= bigmask - 1;
+    const uint32_t nqj = __shfl_sync(0xffffffffu, nq, j);
+    const uint32_t sbj = __shfl_sync(0xffffffffu, sb, j);
+    double mom[TS_NMOM];
+#pragma unroll
+    for (int k = 0; k < TS_NMOM; k++) mom[k] = 0.0;
+    uint32_t cnt = 0, scnt = 0;
+    accumulate_slots(partial, flag, sbj, sbj + nqj, lane, 32, mom, cnt, scnt);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int k = 0; k < TS_NMOM; k++) mom[k] += __shfl_xor_sync(0xffffffffu, mom[k], d);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+      scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
+    }
+    if (lane == j)
+      store_motion(m, gv, solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels,
+                                        min_weight));
+  }
   }
 }
 
@@ -191,11 +280,23 @@ static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) 
 
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
-                     const ts_config &cfg, ts_motions m, cudaStream_t s) {
-  if (nv_total)
+                     const ts_config &cfg, ts_motions m, const uint8_t *touched, uint32_t *list,
+                     uint32_t *n_list, cudaStream_t s) {
+  if (!nv_total) return;
+  if (!touched) {  // no touched bytes (K2's legacy loop): every gv walks its flags
     k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, bbox, nv_total,
                                                    cfg.det_floor, cfg.min_pixels, cfg.min_weight,
                                                    m);
+    return;
+  }
+  cudaMemsetAsync(n_list, 0, sizeof(uint32_t), s);
+  k3_defaults<<<blocks(nv_total, 256), 256, 0, s>>>(touched, nv_total, m, list, n_list);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(blocks(nv_total, 256), (int64_t)sms * 8);
+  k3_solve_list<<<(unsigned)grid, 256, 0, s>>>(partial, flag, inst_base, bbox, list, n_list,
+                                               cfg.det_floor, cfg.min_pixels, cfg.min_weight, m);
 }
 
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
