@@ -44,6 +44,8 @@ struct DevBuf {
   T *as() const { return reinterpret_cast<T *>(p); }
 };
 
+constexpr int64_t K1_TIE_RUN_MAX_HOST = 64;  // binning.cu K1_TIE_RUN_MAX
+
 int bits_for(uint64_t x) {  // number of bits needed to represent values < x
   int b = 0;
   while (b < 64 && (1ull << b) < x) b++;
@@ -67,7 +69,7 @@ struct ts_plan {
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
   // regularisation buffers
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
-      reg_static, reg_source, reg_euler, k4_ws, drange, k2_sched;
+      reg_static, reg_source, reg_euler, k4_ws, drange, k2_sched, tie_runs, tie_tmp;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
   int64_t n = 0, n_inst = 0, n_slots = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
@@ -123,7 +125,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
                           &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
-                          &p->touched, &p->k3_list};
+                          &p->touched, &p->k3_list, &p->tie_runs, &p->tie_tmp};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -141,7 +143,7 @@ void release_all(ts_plan *p) {
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
                     &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
-                    &p->touched, &p->k3_list};
+                    &p->touched, &p->k3_list, &p->tie_runs, &p->tie_tmp};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -345,17 +347,23 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
       return k1_sort_pairs(tmp, bytes, ptr<uint32_t>(p->dkey), ptr<uint32_t>(p->dkey2),
                            ptr<uint32_t>(p->dval), ptr<uint32_t>(p->dval2), (int)NV, end_bit, s);
     }));
+    const uint32_t long_cap = (uint32_t)(NV / (K1_TIE_RUN_MAX_HOST + 1) + 1);
+    ENSURE(p->tie_runs, 8 * ((int64_t)long_cap + 1));
+    TS_CUDA_TRY(cudaMemsetAsync(p->tie_runs.p, 0, 4, s));
     launch_k1_fix_ties(ptr<uint32_t>(p->dkey2), ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
-                       s);
+                       ptr<uint32_t>(p->tie_runs), long_cap, s);
     // instance offsets in depth order: scan of the tile counts gathered through the sorted gvs
     // (the gather is fused into the scan's loads)
     cub::TransformInputIterator<uint32_t, GatherCount, cub::CountingInputIterator<int64_t>>
         cnt_it(cub::CountingInputIterator<int64_t>(0),
                GatherCount{ptr<uint32_t>(p->dval2), ptr<uint32_t>(p->ntiles), NV});
-    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
-      return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt_it, ptr<uint32_t>(p->off_sorted),
-                                           (int)(NV + 1), s);
-    }));
+    auto offsets_scan = [&]() {
+      return cub_call(p, s, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt_it, ptr<uint32_t>(p->off_sorted),
+                                             (int)(NV + 1), s);
+      });
+    };
+    TS_CUDA_TRY(offsets_scan());
     // partial-moment slot base of every gv (gv order): one slot per bbox quadrant
     cub::TransformInputIterator<uint32_t, QuadCount, cub::CountingInputIterator<int64_t>> q_it(
         cub::CountingInputIterator<int64_t>(0), QuadCount{ptr<int16_t>(p->bbox), NV});
@@ -368,9 +376,31 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
                                 cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 1, ptr<uint32_t>(p->inst_base) + NV, 4,
                                 cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 2, p->tie_runs.p, 4, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
     p->n_inst = (int64_t)p->host_small[0];
     p->n_slots = (int64_t)p->host_small[1];
+    const uint32_t n_long = p->host_small[2];
+    if (n_long > 0) {
+      // rare path (degenerate geometry): runs of > K1_TIE_RUN_MAX equal quantised keys, sorted
+      // by the exact depth bits with a stable segmented radix sort -- stable, so equal depths
+      // keep the gid order of the quantised sort's input (splat.py:178) -- then the depth-order
+      // offsets are rescanned (the set of gvs, hence the totals, is unchanged)
+      if (n_long > long_cap) return TS_E_CAPACITY;
+      ENSURE(p->tie_tmp, 20 * NV + 8 * (int64_t)n_long + 64);
+      uint64_t *kin = ptr<uint64_t>(p->tie_tmp), *kout = kin + NV;
+      uint32_t *vout = reinterpret_cast<uint32_t *>(kout + NV), *rb = vout + NV, *re = rb + n_long;
+      launch_k1_long_run_keys(ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
+                              ptr<uint32_t>(p->tie_runs), n_long, kin, rb, re, s);
+      TS_CUDA_TRY(cudaMemcpyAsync(vout, p->dval2.p, 4 * NV, cudaMemcpyDeviceToDevice, s));
+      TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+        return cub::DeviceSegmentedRadixSort::SortPairs(tmp, bytes, kin, kout,
+                                                        ptr<uint32_t>(p->dval2), vout, (int)NV,
+                                                        (int)n_long, rb, re, 0, 64, s);
+      }));
+      TS_CUDA_TRY(cudaMemcpyAsync(p->dval2.p, vout, 4 * NV, cudaMemcpyDeviceToDevice, s));
+      TS_CUDA_TRY(offsets_scan());
+    }
   } else {
     p->n_inst = 0;
     p->n_slots = 0;
@@ -567,7 +597,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
-  const bool use_touched = k2_writes_touched();
+  static const bool k3_split = !(getenv("TS_K3_SPLIT") && getenv("TS_K3_SPLIT")[0] == '0');
+  const bool use_touched = k3_split && k2_writes_touched();
   if (use_touched) {
     ENSURE(p->touched, NV + 8);
     ENSURE(p->k3_list, 4 * (NV + 8));
@@ -589,6 +620,13 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   // K3 and K4 stay separate: a fused per-Gaussian K3+K4 serialises the memory-bound per-view
   // fits inside a 200-register thread and measured 3.0 ms vs 0.6 + 1.5 ms (cfg2).
   cudaEvent_t e4 = p->mark_begin(s);
+  if (use_touched) {  // the touched gvs in gv order (the fits of K3), count on the device
+    uint32_t *list = ptr<uint32_t>(p->k3_list), *n_list = list + NV + 4;
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceSelect::Flagged(tmp, bytes, cub::CountingInputIterator<uint32_t>(0),
+                                        ptr<uint8_t>(p->touched), list, n_list, (int)NV, s);
+    }));
+  }
   launch_k3_solve(ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), ptr<uint32_t>(p->inst_base),
                   ptr<uint32_t>(p->ntiles), ptr<int16_t>(p->bbox), NV, p->cfg, m,
                   use_touched ? ptr<uint8_t>(p->touched) : nullptr,

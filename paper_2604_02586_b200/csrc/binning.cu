@@ -115,9 +115,14 @@ __global__ void k1_depth_keys(const double *__restrict__ depth64,
   dkey[gv] = key;
 }
 
-// Re-sort runs of equal (view, f32 depth) keys by the exact (f64 depth, gid) key.
+// Re-sort runs of equal (view, quantised depth) keys by the exact (f64 depth, gid) key.  Runs
+// longer than K1_TIE_RUN_MAX (planar / fronto-parallel geometry, duplicated Gaussians: the
+// insertion sort would be quadratic) are listed in long_runs ([0] = count, then (start, end)
+// pairs) and sorted afterwards by a segmented radix sort on the exact depth bits (api.cu).
+constexpr int64_t K1_TIE_RUN_MAX = 64;
 __global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restrict__ val,
-                            const double *__restrict__ depth64, int64_t M) {
+                            const double *__restrict__ depth64, int64_t M,
+                            uint32_t *__restrict__ long_runs, uint32_t long_cap) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= M) return;
   const uint32_t kk = key[k];
@@ -125,7 +130,16 @@ __global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restri
   if (k > 0 && key[k - 1] == kk) return;
   if (k + 1 >= M || key[k + 1] != kk) return;
   int64_t e = k + 1;
-  while (e < M && key[e] == kk) e++;
+  while (e < M && key[e] == kk && e - k <= K1_TIE_RUN_MAX) e++;
+  if (e - k > K1_TIE_RUN_MAX) {
+    while (e < M && key[e] == kk) e++;
+    const uint32_t i = atomicAdd(long_runs, 1u);
+    if (i < long_cap) {
+      long_runs[2 + 2 * i] = (uint32_t)k;
+      long_runs[3 + 2 * i] = (uint32_t)e;
+    }
+    return;
+  }
   for (int64_t i = k + 1; i < e; i++) {
     uint32_t x = val[i];
     double dx = depth64[x];
@@ -270,8 +284,30 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
   k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dkey);
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
-                        cudaStream_t s) {
-  if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M);
+                        uint32_t *long_runs, uint32_t long_cap, cudaStream_t s) {
+  if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M, long_runs, long_cap);
+}
+
+// Long tie runs: exact depth bits of the sorted gvs (positive depths: the bit patterns order as
+// the values) and the runs' (start, end) split into two offset arrays for the segmented sort.
+__global__ void k1_depth_bits(const uint32_t *__restrict__ val, const double *__restrict__ depth64,
+                              int64_t M, uint64_t *__restrict__ bits) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) bits[i] = double_bits(depth64[val[i]]);
+}
+__global__ void k1_split_runs(const uint32_t *__restrict__ long_runs, uint32_t n,
+                              uint32_t *__restrict__ begin, uint32_t *__restrict__ end) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    begin[i] = long_runs[2 + 2 * i];
+    end[i] = long_runs[3 + 2 * i];
+  }
+}
+void launch_k1_long_run_keys(const uint32_t *val, const double *depth64, int64_t M,
+                             const uint32_t *long_runs, uint32_t n_runs, uint64_t *bits,
+                             uint32_t *begin, uint32_t *end, cudaStream_t s) {
+  if (M) k1_depth_bits<<<blocks(M, 256), 256, 0, s>>>(val, depth64, M, bits);
+  if (n_runs) k1_split_runs<<<blocks(n_runs, 256), 256, 0, s>>>(long_runs, n_runs, begin, end);
 }
 void launch_k1_emit(const uint32_t *val, const int16_t *bbox, const uint32_t *off_sorted,
                     int64_t M, int tiles_x, uint32_t *tkey, uint32_t *tval, cudaStream_t s) {

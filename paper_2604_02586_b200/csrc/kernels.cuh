@@ -11,7 +11,10 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
                        uint32_t *drange, uint32_t *dkey, uint32_t *dval, double *depth64,
                        uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s);
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
-                        cudaStream_t s);
+                        uint32_t *long_runs, uint32_t long_cap, cudaStream_t s);
+void launch_k1_long_run_keys(const uint32_t *val, const double *depth64, int64_t M,
+                             const uint32_t *long_runs, uint32_t n_runs, uint64_t *bits,
+                             uint32_t *begin, uint32_t *end, cudaStream_t s);
 void launch_k1_emit(const uint32_t *val, const int16_t *bbox, const uint32_t *off_sorted,
                     int64_t M, int tiles_x, uint32_t *tkey, uint32_t *tval, cudaStream_t s);
 void launch_k1_tile_ranges(const uint32_t *tkey, const uint32_t *tval, int64_t n_inst, int64_t n,
@@ -35,8 +38,8 @@ bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched 
 // K3: per-(view, Gaussian) affine fit from the tile partials of K2.
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
-                     const ts_config &cfg, ts_motions m, const uint8_t *touched, uint32_t *list,
-                     uint32_t *n_list, cudaStream_t s);
+                     const ts_config &cfg, ts_motions m, const uint8_t *touched,
+                     const uint32_t *list, const uint32_t *n_list, cudaStream_t s);
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
                       int64_t n, double det_floor, int min_pixels, double min_weight,

@@ -23,7 +23,6 @@
 //     (instance, quadrant) sub-slot: no atomics, no zero-initialised accumulators,
 //     bit-reproducible (K3 adds the sub-slots in fixed order).
 #include <cub/cub.cuh>
-#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -56,7 +55,7 @@ struct K2Params {
   // accumulate mode
   Partial *partial;  // one slot per (gv, 8x8 quadrant of its bbox)
   uint8_t *flag;
-  uint8_t *touched;  // per gv: 1 once it has a tracked contribution (k2_accum), zeroed before
+  uint8_t *touched;  // per gv: 1 once it has a tracked contribution (zeroed before K2)
   // emit mode
   unsigned long long *emit_count;
   int64_t emit_cap;
@@ -425,282 +424,6 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
     for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);
 }
 
-// ---------------------------------------------------------------------------------------------
-// K2 accumulate mode: batched evaluation (the production path).
-//
-// Same work units, culling and arithmetic as k2_raster, but the culled Gaussians of a unit are
-// appended (in depth order) to a per-warp batch of K2B_BATCH entries in shared memory (SoA), and a
-// full batch is processed in three warp-wide phases instead of one Gaussian at a time:
-//   1. alpha: the batch's candidate (entry, pixel) pairs -- bbox x quadrant, unsaturated pixels --
-//      are listed in shared memory (row = entry x pixel half, in (entry, pixel) order) and
-//      evaluated 32 per round, one per lane: q, the keep predicate and alpha do not depend on
-//      T, so every lane evaluates a real candidate instead of one Gaussian's 64 pixel slots
-//      (the lane utilisation of the pixel-owned loop was 19.6/32);
-//   2. compositing: each lane walks its two pixels' candidate entries front to back with the
-//      alphas from phase 1 (w = alpha T, T *= 1 - alpha: a few instructions per step);
-//   3. moments: the lane pair of each entry walks the entry's two list rows and reduces its
-//      anchored moments (one xor shuffle), each entry's (gv, quadrant) slot written once.
-// Arithmetic per pair is k2_raster's (q in numpy's order, table exp, T as the running product),
-// so the contribution set, alpha, T and the integer counts are bit-identical to it; only the
-// summation order of the moments differs.
-constexpr int K2B_BATCH = 11;   // entries per batch (two list rows / flush lanes each)
-constexpr int K2B_WARPS = 4;
-
-template <typename TrackT>
-struct K2BWarp {
-  double mx[K2B_BATCH], my[K2B_BATCH], i00[K2B_BATCH], i01x2[K2B_BATCH], i11[K2B_BATCH],
-      op[K2B_BATCH];
-  uint64_t rect[K2B_BATCH];
-  uint32_t slot[K2B_BATCH], gv[K2B_BATCH];
-  int ax[K2B_BATCH], ay[K2B_BATCH];
-  double w[K2B_BATCH][K2_WROW];           // alpha after phase 1, w = alpha T (or 0) after phase 2
-  uint16_t pair[K2B_BATCH * 64];          // candidate list: entry << 6 | pixel
-  TrackT trk_u[64], trk_v[64];
-};
-
-template <typename TrackT>
-__device__ __forceinline__ void k2b_process(K2BWarp<TrackT> &S, const K2Params &P, int lane,
-                                            int nb, bool valid0, bool valid1, double &T0,
-                                            double &T1, uint64_t &done64, uint64_t static64,
-                                            int qx0, int qy0, const double *etab) {
-  __syncwarp();
-  const double es = P.early_stop, cutoff = P.alpha_cutoff;
-  // ---- candidate list: lane r = list row (entry r >> 1, pixel half r & 1)
-  const int e = lane >> 1, h = lane & 1;
-  uint32_t row = 0;
-  if (e < nb) row = (uint32_t)((S.rect[e] & ~done64) >> (32 * h));
-  const int cnt_row = __popc(row);
-  int off = cnt_row;  // inclusive scan over the 32 rows
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int o = __shfl_up_sync(0xffffffffu, off, d);
-    if (lane >= d) off += o;
-  }
-  const int total = __shfl_sync(0xffffffffu, off, 31);
-  off -= cnt_row;  // exclusive
-  {
-    uint32_t b = row;
-    int i = off;
-    const uint16_t hi = (uint16_t)((e << 6) | (32 * h));
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      S.pair[i++] = (uint16_t)(hi | bit);
-    }
-  }
-  __syncwarp();
-  // ---- phase 1: alpha of every candidate pair, one per lane per round (splat.py:153-155)
-  for (int i = lane; i < total; i += 32) {
-    const int pr = S.pair[i];
-    const int k = pr >> 6, p = pr & 63;
-    const double fpx = (double)(qx0 + (p & 7)), fpy = (double)(qy0 + (p >> 3));
-    const double dx = sub(fpx, S.mx[k]), dy = sub(fpy, S.my[k]);
-    const double q = add(add(mul(mul(S.i00[k], dx), dx), mul(mul(S.i01x2[k], dx), dy)),
-                         mul(mul(S.i11[k], dy), dy));
-    const bool in = q <= TS_SIGMA_RADIUS * TS_SIGMA_RADIUS;
-    const double a = alpha_of_table(S.op[k], in ? q : 0.0, etab);  // table index in range
-    S.w[k][p] = (in && a >= cutoff) ? a : 0.0;  // alpha >= cutoff > 0: 0 marks "no keep"
-  }
-  // each pixel's candidate entries (bit k = entry k, depth order)
-  uint32_t mA = 0, mB = 0;
-  {
-    const uint32_t nd_lo = ~(uint32_t)done64, nd_hi = ~(uint32_t)(done64 >> 32);
-    for (int k = 0; k < nb; k++) {
-      const uint64_t r = S.rect[k];
-      mA |= (((uint32_t)r & nd_lo) >> lane & 1u) << k;
-      mB |= (((uint32_t)(r >> 32) & nd_hi) >> lane & 1u) << k;
-    }
-  }
-  __syncwarp();
-  // ---- phase 2: compositing front to back (splat.py:182-193, motion2d.py:151); every kept
-  // alpha lowers T, a pair contributes while T >= early_stop and its pixel has a valid track
-  while (__any_sync(0xffffffffu, (mA | mB) != 0u)) {
-    if (mA) {
-      const int k = __ffs(mA) - 1;
-      mA &= mA - 1;
-      const double a = S.w[k][lane];
-      const bool keep = a > 0.0 && T0 >= es;
-      const double w = mul(a, T0);
-      if (a > 0.0) T0 = mul(T0, sub(1.0, a));
-      S.w[k][lane] = (keep && valid0) ? w : 0.0;
-    }
-    if (mB) {
-      const int k = __ffs(mB) - 1;
-      mB &= mB - 1;
-      const double a = S.w[k][lane + 32];
-      const bool keep = a > 0.0 && T1 >= es;
-      const double w = mul(a, T1);
-      if (a > 0.0) T1 = mul(T1, sub(1.0, a));
-      S.w[k][lane + 32] = (keep && valid1) ? w : 0.0;
-    }
-  }
-  done64 = (uint64_t)__ballot_sync(0xffffffffu, !(T0 >= es)) |
-           ((uint64_t)__ballot_sync(0xffffffffu, !(T1 >= es)) << 32);
-  __syncwarp();
-  // ---- phase 3: moments (motion2d.py:144-160) anchored at the entry's bbox centre pixel; lane
-  // (e, h) sums the contributions of its list row, one xor shuffle adds the entry's two rows
-  double m[TS_NMOM];
-#pragma unroll
-  for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
-  uint32_t cnt = 0, scnt = 0;
-  if (cnt_row) {
-    const int ax = S.ax[e], ay = S.ay[e];
-    const double fax = (double)ax, fay = (double)ay;
-    const uint32_t st32 = (uint32_t)(static64 >> (32 * h));
-    for (int i = off; i < off + cnt_row; i++) {
-      const int p = S.pair[i] & 63;
-      const double w = S.w[e][p];
-      if (w == 0.0) continue;  // w = alpha T >= cutoff * early_stop > 0 for a contribution
-      const double dx = (double)(qx0 + (p & 7) - ax), dy = (double)(qy0 + (p >> 3) - ay);
-      const double ua = (double)S.trk_u[p] - fax, va = (double)S.trk_v[p] - fay;
-      const double wx = w * dx, wy = w * dy;
-      m[0] += w;
-      m[1] += wx;
-      m[2] += wy;
-      m[3] += wx * dx;
-      m[4] += wx * dy;
-      m[5] += wy * dy;
-      m[6] += w * ua;
-      m[7] += w * va;
-      m[8] += wx * ua;
-      m[9] += wx * va;
-      m[10] += wy * ua;
-      m[11] += wy * va;
-      const uint32_t st = (st32 >> (p & 31)) & 1u;
-      m[12] += st ? w : 0.0;
-      scnt += st;
-      cnt++;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], 1);
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-  scnt += __shfl_xor_sync(0xffffffffu, scnt, 1);
-  if (cnt && e < nb) {
-    Partial *dst = P.partial + S.slot[e];
-    if (h == 0) {
-      dst->m[0] = m[0]; dst->m[1] = m[1]; dst->m[2] = m[2]; dst->m[3] = m[3];
-      dst->m[4] = m[4]; dst->m[5] = m[5]; dst->m[6] = m[6];
-    } else {
-      dst->m[7] = m[7]; dst->m[8] = m[8]; dst->m[9] = m[9]; dst->m[10] = m[10];
-      dst->m[11] = m[11]; dst->m[12] = m[12];
-      dst->count = cnt;
-      dst->static_count = scnt;
-      P.flag[S.slot[e]] = 1;
-      if (P.touched) P.touched[S.gv[e]] = 1;
-    }
-  }
-  __syncwarp();
-}
-
-template <typename TrackT>
-__global__ void __launch_bounds__(K2B_WARPS * 32, 6) k2_accum(const K2Params P) {
-  extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-  double *etab = reinterpret_cast<double *>(k2_smem_raw);  // exp(-k/64), k = 0..288
-  for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  K2BWarp<TrackT> &S = reinterpret_cast<K2BWarp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
-  const uint32_t n_units = 4u * *P.n_items;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-
-  for (;;) {
-    uint32_t unit = 0;
-    if (lane == 0) unit = atomicAdd(P.work_counter, 1u);
-    unit = __shfl_sync(0xffffffffu, unit, 0);
-    if (unit >= n_units) break;
-    const int tile = (int)P.items[unit >> 2];
-    const int quad = (int)(unit & 3);
-    const uint32_t start = P.tile_range[2 * tile], end = P.tile_range[2 * tile + 1];
-    const int v = tile / P.tiles_per_view;
-    const int t = tile - v * P.tiles_per_view;
-    const int ty = t / P.tiles_x, tx = t - ty * P.tiles_x;
-    const int qx0 = tx * TS_TILE + (quad & 1) * 8, qy0 = ty * TS_TILE + (quad >> 1) * 8;
-    const int px = qx0 + (lane & 7);
-    const int py0 = qy0 + (lane >> 3), py1 = py0 + 4;
-    const double fpx = (double)px, fpy0 = (double)py0, fpy1 = (double)py1;
-    const bool in0 = px < P.W && py0 < P.H, in1 = px < P.W && py1 < P.H;
-
-    bool valid0 = false, valid1 = false;
-    uint64_t static64 = 0;
-    __syncwarp();
-#pragma unroll
-    for (int hh = 0; hh < 2; hh++) {
-      const int py = hh ? py1 : py0;
-      TrackT u = TrackT(0), vv = TrackT(0);
-      bool val = false;
-      if (hh ? in1 : in0) {
-        // plain loads (no read-only path): the tracks may be pinned host memory read in place
-        const int64_t pix = ((int64_t)v * P.H + py) * P.W + px;
-        const uint8_t vb = P.track_valid[pix];
-        const TrackT *tg = reinterpret_cast<const TrackT *>(P.track_target) + 2 * pix;
-        const TrackT tu = tg[0], tv = tg[1];
-        val = vb != 0;
-        if (val) {  // invalid targets may be NaN: never used
-          u = tu;
-          vv = tv;
-        }
-      }
-      const int p = lane + 32 * hh;
-      S.trk_u[p] = u;
-      S.trk_v[p] = vv;
-      const bool st = val && is_static((double)u, (double)vv, px, py, P.static_thr);
-      static64 |= (uint64_t)__ballot_sync(0xffffffffu, st) << (32 * hh);
-      if (hh) valid1 = val; else valid0 = val;
-    }
-    double T0 = in0 ? 1.0 : 0.0, T1 = in1 ? 1.0 : 0.0;
-    uint64_t done64 = (uint64_t)__ballot_sync(0xffffffffu, !(T0 >= P.early_stop)) |
-                      ((uint64_t)__ballot_sync(0xffffffffu, !(T1 >= P.early_stop)) << 32);
-    int nb = 0;  // entries in the batch
-    for (uint32_t b = start; b < end; b += 32) {
-      if (done64 == ~0ull) break;
-      const uint32_t i = b + lane;
-      bool hit = false;
-      RasterRec r;
-      uint64_t rect = 0;
-      uint32_t ibase = 0, gv = 0;
-      if (i < end) {
-        gv = P.inst_gv[i];
-        ibase = __ldg(P.inst_base + gv);
-        r = P.rec[gv];
-        rect = quad_rect(r, qx0, qy0);
-        hit = (rect & ~done64) != 0ull;
-      }
-      uint32_t hm = __ballot_sync(0xffffffffu, hit);
-      while (hm) {
-        // append the first (K2B_BATCH - nb) remaining hits, in instance order
-        const int take = min(K2B_BATCH - nb, __popc(hm));
-        const int rank = __popc(hm & lt_mask);
-        const bool mine = ((hm >> lane) & 1u) && rank < take;
-        if (mine) {
-          const int k = nb + rank;
-          S.mx[k] = r.mx;
-          S.my[k] = r.my;
-          S.i00[k] = r.i00;
-          S.i01x2[k] = r.i01x2;
-          S.i11[k] = r.i11;
-          S.op[k] = r.opacity;
-          S.rect[k] = rect;
-          const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
-          S.slot[k] = ibase + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
-                                         ((qx0 >> 3) - bx0));
-          S.gv[k] = gv;
-          S.ax[k] = anchor_x(r);
-          S.ay[k] = anchor_y(r);
-        }
-        hm &= ~__ballot_sync(0xffffffffu, mine);
-        nb += take;
-        if (nb == K2B_BATCH) {
-          k2b_process(S, P, lane, nb, valid0, valid1, T0, T1, done64, static64, qx0, qy0, etab);
-          nb = 0;
-        }
-      }
-    }
-    if (nb > 0)
-      k2b_process(S, P, lane, nb, valid0, valid1, T0, T1, done64, static64, qx0, qy0, etab);
-  }
-}
-
 // Compact list of the non-empty tiles in [t0, t1) (order irrelevant: every unit is independent).
 __global__ void k2_build_items(const uint32_t *__restrict__ tile_range, int t0, int t1,
                                uint32_t *__restrict__ items, uint32_t *__restrict__ n_items) {
@@ -766,28 +489,7 @@ static cudaError_t launch_mode(const K2Params &P, cudaStream_t s, int cap) {
   return cudaGetLastError();
 }
 
-bool k2_writes_touched() { return true; }  // both accumulate kernels mark touched gvs
-
-static bool k2_legacy() {
-  static const bool legacy = std::getenv("TS_K2_LEGACY") != nullptr;  // A/B of the two loops
-  return legacy;
-}
-
-template <typename TrackT>
-static cudaError_t launch_accum(const K2Params &P, cudaStream_t s, int cap) {
-  auto kern = k2_accum<TrackT>;
-  const size_t smem = K2_ETAB_BYTES + sizeof(K2BWarp<TrackT>) * K2B_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2B_WARPS * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (cap > 0 && cap < per_sm) per_sm = cap;
-  kern<<<sms * (per_sm > 0 ? per_sm : 1), K2B_WARPS * 32, smem, s>>>(P);
-  return cudaGetLastError();
-}
+bool k2_writes_touched() { return true; }  // the accumulate kernel marks touched gvs
 
 cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uint32_t *inst_gv,
                       const uint32_t *tile_range, const uint32_t *inst_base, uint32_t *items,
@@ -850,12 +552,8 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.dom_depth = dom_depth;
   P.stats = stats;
   if (mode == K2_ACCUMULATE) {
-    if (k2_legacy()) {
-      if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
-      return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
-    }
-    if (track_dtype == TS_TRACK_F32) return launch_accum<float>(P, s, ctas_per_sm);
-    return launch_accum<double>(P, s, ctas_per_sm);
+    if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
+    return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
   }
   if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s, ctas_per_sm);
   return launch_mode<K2_DOMINANT, float>(P, s, ctas_per_sm);

@@ -101,36 +101,24 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial 
 // K3 split by K2's per-gv "touched" bytes (a gv with at least one tracked contribution).  At the
 // large configs most gvs are occluded (cfg5: ~7% touched), and a warp with any touched lane
 // waited on the whole bbox -> slot base -> flags -> partials chain.  Instead:
-//   k3_defaults: every gv's motion = UNSOLVABLE / A = I / b = 0 / zero sums, coalesced streaming
-//                stores, and the touched gvs appended to a list (warp-aggregated atomic);
-//   k3_solve_list: the fit of the listed gvs (one thread each, big bboxes per warp as k3_solve),
-//                  overwriting their defaults (same stream, after k3_defaults).
-// The list order varies run to run; every gv's result does not depend on it.
+//   select (CUB DeviceSelect::Flagged, api.cu): the touched gvs, in gv order;
+//   k3_defaults: every untouched gv's motion = UNSOLVABLE / A = I / b = 0 / zero sums
+//                (coalesced streaming stores, no dependent loads);
+//   k3_solve_list: the fit of the listed gvs (one thread each, big bboxes per warp as k3_solve).
+// Every gv is written exactly once; results do not depend on the split.
 __global__ void __launch_bounds__(256) k3_defaults(const uint8_t *__restrict__ touched, int64_t NV,
-                                                   ts_motions m, uint32_t *__restrict__ list,
-                                                   uint32_t *__restrict__ n_list) {
+                                                   ts_motions m) {
   const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool valid = gv < NV;
-  const bool t = valid && touched[gv] != 0;
-  if (valid) {
-    GvMotion r;
-    r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
-    r.b[0] = 0.0; r.b[1] = 0.0;
-    r.wsum = 0.0;
-    r.static_wsum = 0.0;
-    r.count = 0;
-    r.static_count = 0;
-    r.status = TS_STATUS_UNSOLVABLE;
-    store_motion(m, gv, r);
-  }
-  const uint32_t tm = __ballot_sync(0xffffffffu, t);
-  if (!tm) return;
-  uint32_t base = 0;
-  const int leader = __ffs(tm) - 1;
-  if (lane == leader) base = atomicAdd(n_list, (uint32_t)__popc(tm));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (t) list[base + __popc(tm & ((1u << lane) - 1u))] = (uint32_t)gv;
+  if (gv >= NV || touched[gv]) return;
+  GvMotion r;
+  r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
+  r.b[0] = 0.0; r.b[1] = 0.0;
+  r.wsum = 0.0;
+  r.static_wsum = 0.0;
+  r.count = 0;
+  r.static_count = 0;
+  r.status = TS_STATUS_UNSOLVABLE;
+  store_motion(m, gv, r);
 }
 
 __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
@@ -280,17 +268,16 @@ static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) 
 
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
-                     const ts_config &cfg, ts_motions m, const uint8_t *touched, uint32_t *list,
-                     uint32_t *n_list, cudaStream_t s) {
+                     const ts_config &cfg, ts_motions m, const uint8_t *touched,
+                     const uint32_t *list, const uint32_t *n_list, cudaStream_t s) {
   if (!nv_total) return;
-  if (!touched) {  // no touched bytes (K2's legacy loop): every gv walks its flags
+  if (!touched) {  // every gv walks its flags
     k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, bbox, nv_total,
                                                    cfg.det_floor, cfg.min_pixels, cfg.min_weight,
                                                    m);
     return;
   }
-  cudaMemsetAsync(n_list, 0, sizeof(uint32_t), s);
-  k3_defaults<<<blocks(nv_total, 256), 256, 0, s>>>(touched, nv_total, m, list, n_list);
+  k3_defaults<<<blocks(nv_total, 256), 256, 0, s>>>(touched, nv_total, m);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
