@@ -499,6 +499,107 @@ def run_ours(args):
     return line
 
 
+def run_clip(args):
+    """Strong scaling over a short clip (BASELINE configs[3]/[4]: 8 target frames sharded over
+    1/2/4/8 GPUs; reference pipeline.py:64-65, :191-196): a step is the clip's T target frames,
+    frame f on rank (f-1) mod world (distributed.frames_for_rank); each rank bins frame 0 ONCE per
+    step and runs K2-K4 for each of its frames on that binning, and every frame's updates are
+    gathered to rank 0 over NCCL on a side stream while the rank's next frame computes.
+    value = T * N * V / (max over ranks of the step time)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02586_b200.distributed import frames_for_rank
+    from paper_2604_02586_b200.engine import FrameEngine
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.config]
+    seed, n, nv = c["args"]
+    gap, T = c["gap"], args.clip_frames
+    targets = [gap * (j + 1) for j in range(T)]
+    mine = frames_for_rank(targets, rank, world)
+    scene, tracks = make_inputs(args.config, gap * T + 1, f"[rank {rank}] ", frames=mine)
+    dev = torch.device("cuda", local)
+    g_dev = torch.as_tensor(scene.frames[0], device=dev)
+    if world > 1:
+        dist.broadcast(g_dev, 0)
+    cams = scene.cameras
+    eng = FrameEngine()
+    stream = torch.cuda.current_stream()
+    gather_stream = torch.cuda.Stream()
+    eng.bin(g_dev, cams)
+    outs = {f: eng.alloc_outputs() for f in mine}
+    slots = max(len(frames_for_rank(targets, r, world)) for r in range(world))
+    bufs = None
+    if world > 1:
+        bufs = [[[torch.empty_like(t) for _ in range(world)]
+                 for t in (outs[mine[0]].delta_mean, outs[mine[0]].rotation,
+                           outs[mine[0]].scale, outs[mine[0]].status)] for _ in range(slots)]
+    gathered = [None] * slots
+
+    def step():
+        eng.bin(g_dev, cams)  # once per clip step, shared by this rank's frames
+        for j in range(slots):
+            if j < len(mine):
+                if gathered[j] is not None:
+                    stream.wait_event(gathered[j])  # outputs reusable once gathered
+                f = mine[j]
+                o = eng.compensate(tracks[f][0], tracks[f][1], outs[f])
+                ts = (o.delta_mean, o.rotation, o.scale, o.status)
+            else:  # ranks with fewer frames still join every gather
+                o = outs[mine[0]]
+                ts = (o.delta_mean, o.rotation, o.scale, o.status)
+            if world > 1:
+                gather_stream.wait_stream(stream)
+                with torch.cuda.stream(gather_stream):
+                    for t, b in zip(ts, bufs[j]):
+                        dist.gather(t, b if rank == 0 else None, dst=0)
+                gathered[j] = torch.cuda.Event()
+                gathered[j].record(gather_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        clk.wait_live()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        stream.wait_stream(gather_stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    line = None
+    if rank == 0:
+        cfg = config_dict(args.config, scene)
+        cfg["target_frame"] = f"clip of {T} target frames (frame 0 -> {targets[0]}..{targets[-1]})"
+        cfg["step"] = (f"one clip: K1 binning once per rank, then K2-K4 for each of the rank's "
+                       f"target frames; {T} frames over {world} GPU(s)")
+        line = {"metric": METRIC, "value": T * n * nv / (ms / 1e3), "unit": "Gaussian-views/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (generate_scene + GPU oracle tracker, sigma 0)",
+                "config": cfg, "frames_per_s": T / (ms / 1e3),
+                "parallelism": f"frame-sharded x{world} (strong: {T} frames per step)",
+                "frames_per_rank": [len(frames_for_rank(targets, r, world)) for r in range(world)],
+                "gpu_launches": None, "clocks": clk.summary()}
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
 def run_reference(args):
     """Reference arm: the reference algorithm of the ★ path on the host cores (oracle/cpu_arm.py:
     the C / numpy port pinned against the reference's own outputs), whole frames per step, with
@@ -541,8 +642,17 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="whole frames timed for the cpu_baseline of the GPU arm")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--clip-frames", type=int, default=0,
+                    help="strong scaling: a step is a clip of this many target frames sharded "
+                         "over the ranks, binned once per rank (0: weak scaling, one frame pair "
+                         "per rank per step)")
     args = ap.parse_args()
-    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        line = run_reference(args)
+    elif args.clip_frames:
+        line = run_clip(args)
+    else:
+        line = run_ours(args)
     if line is not None:
         print(json.dumps(line), flush=True)
 
