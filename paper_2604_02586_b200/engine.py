@@ -390,11 +390,15 @@ class StreamingEngine:
     K2_CTAS_PER_SM = 3
 
     SWITCH_VOTES = 3  # consecutive steps that must favour the other mode before "auto" switches
+    SETTLE_STEPS = N_ENGINES + 2  # first steps (allocation, plan growth) never feed a period
 
     def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
         torch = _torch()
         self._compute_ms = None  # median of the last in-place step periods ("auto" mode)
         self._periods = []
+        self._copy_ms_meas = None  # median of the last full-copy step periods
+        self._copy_periods = []
+        self._n_timed = 0
         self._last_zero_copy = True
         self._votes = 0
         self._burst = 0
@@ -471,7 +475,10 @@ class StreamingEngine:
         computed = torch.cuda.Event(enable_timing=True)
         computed.record(cs)
         if self.zero_copy_tracks == "auto":
-            self._timing.append((t0, computed, self._burst, t_d is not None and _pinned(t_d)))
+            self._n_timed += 1
+            settled = self._n_timed > self.SETTLE_STEPS
+            self._timing.append((t0, computed, self._burst if settled else -self._n_timed,
+                                 t_d is not None and _pinned(t_d)))
         self._free[i] = computed
         ds = self.d2h_stream
         ds.wait_event(computed)
@@ -518,27 +525,37 @@ class StreamingEngine:
     def _choose_zero_copy(self, g_host, t_host, v_host):
         if self.zero_copy_tracks != "auto":
             return bool(self.zero_copy_tracks)
-        # Fold in the step period (interval between consecutive finished steps; never blocks).
-        # Only periods of steps that read the tracks in place count: a full-copy step's period
-        # contains the copy itself, which would make the copy look affordable (self-reinforcing).
-        # Steps finish on N_ENGINES compute streams, so a period is read once every event of
-        # the window has completed.
+        # Fold in the step periods (interval between consecutive finished steps; never blocks),
+        # one estimate per track mode from windows whose steps all used that mode.  Steps finish
+        # on N_ENGINES compute streams, so a period is read once every event of the window has
+        # completed; windows across a flush (caller's idle time) or within the first
+        # SETTLE_STEPS steps (allocations) are skipped.
         k = self.N_ENGINES
         while len(self._timing) > k and all(t[1].query() for t in self._timing[:k + 1]):
-            first, last = self._timing[0], self._timing[k]
             window = self._timing[:k + 1]
+            first, last = window[0], window[-1]
             self._timing.pop(0)
-            if first[2] != last[2] or not all(t[3] for t in window):
-                continue  # straddles a flush (caller's idle time) or includes a full copy
-            self._periods = (self._periods + [first[1].elapsed_time(last[1]) / k])[-5:]
-            self._compute_ms = sorted(self._periods)[len(self._periods) // 2]  # robust median
+            if first[2] != last[2] or first[2] < 0:
+                continue
+            period = first[1].elapsed_time(last[1]) / k
+            if all(t[3] for t in window):
+                self._periods = (self._periods + [period])[-5:]
+                self._compute_ms = sorted(self._periods)[len(self._periods) // 2]
+            elif not any(t[3] for t in window):
+                self._copy_periods = (self._copy_periods + [period])[-5:]
+                self._copy_ms_meas = sorted(self._copy_periods)[len(self._copy_periods) // 2]
         if self._compute_ms is None:
             return self._last_zero_copy
         copy_ms = (g_host.numel() * g_host.element_size() + t_host.numel() *
                    t_host.element_size() + v_host.numel()) / (self.H2D_GBS * 1e6)
-        # the copy pays off when it hides under the in-place step period; switching needs
-        # SWITCH_VOTES consecutive steps on the other side of a margin (hysteresis)
-        want_zero_copy = not copy_ms < (0.85 if self._last_zero_copy else 0.95) * self._compute_ms
+        if self._last_zero_copy:
+            # reading in place: copy the whole arrays when that copy hides under the period
+            want_zero_copy = not copy_ms < 0.85 * self._compute_ms
+        else:
+            # copying: go back once the copying steps are measured slower than in-place ones
+            # (the copy sits in their period, so the in-place estimate is never refreshed here)
+            want_zero_copy = (self._copy_ms_meas is not None and
+                              self._copy_ms_meas > 1.02 * self._compute_ms)
         if want_zero_copy == self._last_zero_copy:
             self._votes = 0
         else:

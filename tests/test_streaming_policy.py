@@ -39,6 +39,8 @@ def _engine(period_ms, steps=8, in_place=True):
     se._periods = []
     se._last_zero_copy = True
     se._votes = 0
+    se._copy_ms_meas = None
+    se._copy_periods = []
     se._timing = [(_Ev(k * period_ms), _Ev(k * period_ms), 0, in_place) for k in range(steps)]
     return se
 
@@ -117,3 +119,23 @@ def test_period_estimate_is_robust_to_a_slow_first_step():
         [(_Ev(30.0 + 4.0 * k), _Ev(30.0 + 4.0 * k), 0, True) for k in range(1, 12)]
     _choose(se, 100.0)
     assert se._compute_ms == pytest.approx(4.0)
+
+
+def test_warmup_steps_never_feed_the_estimate():
+    """The round-2 driver failure: slow first steps (allocations) inflated the in-place period,
+    the policy switched to copying and froze there.  Unsettled steps carry a negative burst tag
+    and are skipped."""
+    se = _engine(period_ms=4.2, steps=0)
+    se._timing = [(_Ev(40.0 * k), _Ev(40.0 * k), -(k + 1), True) for k in range(5)] + \
+        [(_Ev(200.0 + 4.2 * k), _Ev(200.0 + 4.2 * k), 0, True) for k in range(8)]
+    assert _choose_n(se, 273.0, 4) == [True] * 4
+    assert se._compute_ms == pytest.approx(4.2)
+
+
+def test_copy_mode_returns_when_copies_are_slower():
+    se = _engine(period_ms=4.2, steps=8)
+    _choose(se, 273.0)
+    se._last_zero_copy = False  # e.g. after a transient
+    se._timing = [(_Ev(100.0 + 5.3 * k), _Ev(100.0 + 5.3 * k), 0, False) for k in range(8)]
+    votes = StreamingEngine.SWITCH_VOTES
+    assert _choose_n(se, 273.0, votes) == [False] * (votes - 1) + [True]
