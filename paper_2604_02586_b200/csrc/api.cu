@@ -5,6 +5,8 @@
 // (instance count after binning, contribution count of the emitting rasterizer).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -45,6 +47,9 @@ struct DevBuf {
 };
 
 constexpr int64_t K1_TIE_RUN_MAX_HOST = 64;  // binning.cu K1_TIE_RUN_MAX
+#ifndef TS_K1_KEY_BITS
+#define TS_K1_KEY_BITS 24
+#endif
 
 int bits_for(uint64_t x) {  // number of bits needed to represent values < x
   int b = 0;
@@ -333,7 +338,10 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
 
   cudaEvent_t e0 = p->mark_begin(s);
   ENSURE(p->drange, 8 * 64);
-  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, ptr<RasterRec>(p->rec),
+  // depth key: view bits + quantised depth, TS_K1_KEY_BITS in all (24: three 8-bit onesweep
+  // passes instead of four; the extra ties are repaired by k1_fix_ties)
+  const int dbits = std::min(26, TS_K1_KEY_BITS - bits_for((uint64_t)V));
+  launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, dbits, ptr<RasterRec>(p->rec),
                     ptr<uint32_t>(p->drange), ptr<uint32_t>(p->dkey),
                     ptr<uint32_t>(p->dval), ptr<double>(p->depth64), ptr<uint32_t>(p->ntiles),
                     ptr<int8_t>(p->status), ptr<int16_t>(p->bbox), s);
@@ -342,7 +350,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
 
   cudaEvent_t e1 = p->mark_begin(s);
   if (NV > 0) {
-    const int end_bit = 26 + bits_for((uint64_t)V);
+    const int end_bit = dbits + bits_for((uint64_t)V);
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
       return k1_sort_pairs(tmp, bytes, ptr<uint32_t>(p->dkey), ptr<uint32_t>(p->dkey2),
                            ptr<uint32_t>(p->dval), ptr<uint32_t>(p->dval2), (int)NV, end_bit, s);
@@ -351,7 +359,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
     ENSURE(p->tie_runs, 8 * ((int64_t)long_cap + 1));
     TS_CUDA_TRY(cudaMemsetAsync(p->tie_runs.p, 0, 4, s));
     launch_k1_fix_ties(ptr<uint32_t>(p->dkey2), ptr<uint32_t>(p->dval2), ptr<double>(p->depth64), NV,
-                       ptr<uint32_t>(p->tie_runs), long_cap, s);
+                       dbits, ptr<uint32_t>(p->tie_runs), long_cap, s);
     // instance offsets in depth order: scan of the tile counts gathered through the sorted gvs
     // (the gather is fused into the scan's loads)
     cub::TransformInputIterator<uint32_t, GatherCount, cub::CountingInputIterator<int64_t>>
@@ -563,7 +571,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!p || p->V < 1) return TS_E_INVALID_ARGUMENT;
   if (!updates && !motions) return TS_E_INVALID_ARGUMENT;  // nothing would be returned
   if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
-  const int64_t n = p->n, NV = n * p->V, ni = p->n_inst;
+  const int64_t n = p->n, NV = n * p->V;
   // tracks: device memory, or pinned host memory that K2 reads in place (zero-copy: only the
   // 8x8 quadrants of occupied tiles cross PCIe)
   {

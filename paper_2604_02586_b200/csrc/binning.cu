@@ -96,21 +96,23 @@ __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__
 // mantissa bits a truncated float key keeps (far fewer ties to repair).
 __global__ void k1_depth_keys(const double *__restrict__ depth64,
                               const int8_t *__restrict__ status,
-                              const uint32_t *__restrict__ drange, int64_t n, int V,
+                              const uint32_t *__restrict__ drange, int64_t n, int V, int dbits,
                               uint32_t *__restrict__ dkey) {
   const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gv >= n * V) return;
   const uint32_t v = (uint32_t)(gv / n);
-  uint32_t key = v << 26;
+  const uint32_t sentinel = (1u << dbits) - 1u;
+  uint32_t key = v << dbits;
   if (status[gv] == 3) {
     const double dmin = (double)__uint_as_float(drange[2 * v]);
     const double dmax = (double)__uint_as_float(drange[2 * v + 1]);
     const double span = dmax - dmin;
-    const double scale = span > 0.0 ? 67108862.0 / span : 0.0;
-    const double qd = fmin(fmax((depth64[gv] - dmin) * scale, 0.0), 67108862.0);
+    const double top = (double)(sentinel - 1u);
+    const double scale = span > 0.0 ? top / span : 0.0;
+    const double qd = fmin(fmax((depth64[gv] - dmin) * scale, 0.0), top);
     key |= (uint32_t)qd;
   } else {
-    key |= 0x3FFFFFFu;  // sorts after every binned Gaussian of the view, never emitted
+    key |= sentinel;  // sorts after every binned Gaussian of the view, never emitted
   }
   dkey[gv] = key;
 }
@@ -121,12 +123,13 @@ __global__ void k1_depth_keys(const double *__restrict__ depth64,
 // pairs) and sorted afterwards by a segmented radix sort on the exact depth bits (api.cu).
 constexpr int64_t K1_TIE_RUN_MAX = 64;
 __global__ void k1_fix_ties(const uint32_t *__restrict__ key, uint32_t *__restrict__ val,
-                            const double *__restrict__ depth64, int64_t M,
+                            const double *__restrict__ depth64, int64_t M, int dbits,
                             uint32_t *__restrict__ long_runs, uint32_t long_cap) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= M) return;
   const uint32_t kk = key[k];
-  if ((kk & 0x3FFFFFFu) == 0x3FFFFFFu) return;
+  const uint32_t sentinel = (1u << dbits) - 1u;
+  if ((kk & sentinel) == sentinel) return;
   if (k > 0 && key[k - 1] == kk) return;
   if (k + 1 >= M || key[k + 1] != kk) return;
   int64_t e = k + 1;
@@ -273,19 +276,21 @@ __global__ void k1_range_init(uint32_t *drange, int V) {
   }
 }
 
-void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint32_t *drange, uint32_t *dkey, uint32_t *dval, double *depth64,
-                       uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s) {
+void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, int dbits,
+                       RasterRec *rec, uint32_t *drange, uint32_t *dkey, uint32_t *dval,
+                       double *depth64, uint32_t *ntiles, int8_t *status, int16_t *bbox,
+                       cudaStream_t s) {
   if (n == 0) return;
   k1_range_init<<<1, 64, 0, s>>>(drange, V);
   k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, drange, dval,
                                                                   depth64, ntiles, status, bbox);
   k1_depth_range<<<dim3(16, V), 256, 0, s>>>(depth64, n, drange);
-  k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dkey);
+  k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dbits, dkey);
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
-                        uint32_t *long_runs, uint32_t long_cap, cudaStream_t s) {
-  if (M) k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M, long_runs, long_cap);
+                        int dbits, uint32_t *long_runs, uint32_t long_cap, cudaStream_t s) {
+  if (M)
+    k1_fix_ties<<<blocks(M, 256), 256, 0, s>>>(key, val, depth64, M, dbits, long_runs, long_cap);
 }
 
 // Long tie runs: exact depth bits of the sorted gvs (positive depths: the bit patterns order as

@@ -7,11 +7,12 @@ namespace ts {
 
 enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
 
-void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, RasterRec *rec,
-                       uint32_t *drange, uint32_t *dkey, uint32_t *dval, double *depth64,
-                       uint32_t *ntiles, int8_t *status, int16_t *bbox, cudaStream_t s);
+void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, int dbits,
+                       RasterRec *rec, uint32_t *drange, uint32_t *dkey, uint32_t *dval,
+                       double *depth64, uint32_t *ntiles, int8_t *status, int16_t *bbox,
+                       cudaStream_t s);
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
-                        uint32_t *long_runs, uint32_t long_cap, cudaStream_t s);
+                        int dbits, uint32_t *long_runs, uint32_t long_cap, cudaStream_t s);
 void launch_k1_long_run_keys(const uint32_t *val, const double *depth64, int64_t M,
                              const uint32_t *long_runs, uint32_t n_runs, uint64_t *bits,
                              uint32_t *begin, uint32_t *end, cudaStream_t s);

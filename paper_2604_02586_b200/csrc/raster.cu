@@ -88,8 +88,7 @@ struct K2Warp {
   uint32_t slot[32], gvid[32];
   int2 anc[32];       // moment anchor (bbox centre pixel) of each record (accumulate mode)
   double w[K2_FLUSH][K2_WROW];
-  double2 trk_o[64];  // track target - quadrant origin (exact in double), per pixel
-  double st_o[64];    // 1.0 where the pixel's track is static, else 0.0
+  TrackT trk_u[64], trk_v[64];  // track targets in their input precision
 };
 
 // 64-bit mask (bit = row * 8 + col) of the quadrant pixels inside the record's bbox.
@@ -128,35 +127,36 @@ __device__ __forceinline__ bool eval_pixel(const RasterRec &r, bool cand, double
   return true;
 }
 
-// Transposed reduction of the pending Gaussians (kcount <= K2_FLUSH): the LPG lanes of Gaussian
-// (l & 7) split its contributing pixels by quadrant row (lane qq: rows qq and qq + 4, so an ellipse
-// spreads over all of them), each summing its pixels in pixel order; two xor-shuffle steps add
-// the four partial sums ((s0 + s1) + (s2 + s3): commutative pairs, so all four lanes hold the same
-// bits) and the anchored moments go to the Gaussian's (instance, quadrant) sub-slot.  The
-// per-pixel operands are precomputed per unit (track - quadrant origin, static as 0/1), the
-// counts come from popcounts of the contribution mask.  Warp-uniform call.
+// Transposed reduction of the pending Gaussians (kcount <= K2_FLUSH): lane l sums every fourth
+// contributing pixel of Gaussian (l & 7), starting at its (l >> 3)-th, in pixel order; two
+// xor-shuffle steps add the four partial sums ((s0 + s1) + (s2 + s3): commutative pairs, so all
+// four lanes hold the same bits) and the anchored moments go to the Gaussian's (instance,
+// quadrant) sub-slot.  Warp-uniform call.
 template <typename TrackT>
 __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params &P, int lane,
                                          int kcount, uint64_t my_cm, uint32_t my_slot, int my_ax,
                                          int my_ay, uint64_t static64, int qx0, int qy0) {
-  static_assert(K2_FLUSH == 8, "flush: 8 Gaussians x 4 lanes (one pair of quadrant rows each)");
+  static_assert(K2_FLUSH == 4 || K2_FLUSH == 8, "flush: 4 or 8 Gaussians x 8 or 4 lanes");
+  constexpr int LPG = 32 / K2_FLUSH;  // lanes per pending Gaussian
   const int kk = lane & (K2_FLUSH - 1), qq = lane / K2_FLUSH;
   double m[TS_NMOM];
 #pragma unroll
   for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
-  const uint32_t cnt = (uint32_t)__popcll(my_cm), scnt = (uint32_t)__popcll(my_cm & static64);
+  uint32_t cnt = 0, scnt = 0;
   if (my_cm) {
-    // anchor offsets: x - a = (x - o) + (o - a), all integers, so every operand below is the
-    // exact value of the anchored h = [x - a; 1], x'_a = x' - a (motion2d.py:148-153)
+    const double ax = (double)my_ax, ay = (double)my_ay;
     const double bx = (double)(qx0 - my_ax), by = (double)(qy0 - my_ay);
-    uint64_t bits = my_cm & (0x000000FF000000FFull << (8 * qq));
+    // the LPG lanes of Gaussian kk take every LPG-th of its contributing pixels (lane qq starts
+    // at the qq-th): balanced trip counts whatever the pixels' rows
+    uint64_t bits = my_cm;
+    for (int k = 0; k < qq; k++) bits &= bits - 1;
     while (bits) {
       const int p = __ffsll((long long)bits) - 1;
-      bits &= bits - 1;
+#pragma unroll
+      for (int k = 0; k < LPG; k++) bits &= bits - 1;
       const double w = S.w[kk][p];
       const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
-      const double2 uv = S.trk_o[p];
-      const double ua = uv.x + bx, va = uv.y + by;
+      const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
       const double wx = w * dx, wy = w * dy;
       m[0] += w;
       m[1] += wx;
@@ -170,13 +170,18 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
       m[9] += wx * va;
       m[10] += wy * ua;
       m[11] += wy * va;
-      m[12] = fma(w, S.st_o[p], m[12]);  // + w * 1.0 or + 0.0: exact either way
+      const bool st = (static64 >> p) & 1ull;
+      m[12] += st ? w : 0.0;
+      scnt += st;
+      cnt++;
     }
   }
 #pragma unroll
   for (int d = K2_FLUSH; d < 32; d <<= 1) {
 #pragma unroll
     for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], d);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
   }
   if (kk < kcount && cnt > 0 && qq < 4) {
     // the four lanes of a Gaussian hold identical sums: each stores a quarter of the record
@@ -249,9 +254,9 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
           }
         }
         const int p = lane + 32 * h;
+        S.trk_u[p] = u;
+        S.trk_v[p] = vv;
         const bool st = val && is_static((double)u, (double)vv, px, py, P.static_thr);
-        S.trk_o[p] = make_double2((double)u - (double)qx0, (double)vv - (double)qy0);
-        S.st_o[p] = st ? 1.0 : 0.0;
         static64 |= (uint64_t)__ballot_sync(0xffffffffu, st) << (32 * h);
         if (h) valid1 = val; else valid0 = val;
       }
