@@ -67,7 +67,34 @@ def report(path):
             per.setdefault(key, []).append(f"{d['Metric Name']}: {d['Metric Value']} "
                                            f"{d['Metric Unit']}".rstrip())
     dram = {}
+    extra = {}
     units = dict(zip(rhdr, raw[1])) if len(raw) > 1 else {}
+    pipes = ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+             "smsp__issue_active.avg.pct_of_peak_sustained_active",
+             "smsp__thread_inst_executed_per_inst_executed.ratio"]
+    for r in raw[2:]:
+        d = dict(zip(rhdr, r))
+        key = (d.get("ID"), d.get("Kernel Name"))
+        vals = []
+        for m in pipes:
+            if m in d:
+                vals.append(f"{m.split('.')[0].replace('sm__', '').replace('smsp__', '')}="
+                            f"{d[m]}")
+        stalls = []
+        for m, v in d.items():
+            if m.startswith("smsp__average_warps_issue_stalled_") and \
+                    m.endswith("_per_issue_active.ratio") and "selected" not in m:
+                try:
+                    stalls.append((float(v.replace(",", "")), m[len(
+                        "smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        stalls.sort(reverse=True)
+        extra[key] = (vals, stalls[:4])
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for r in raw[2:]:
         d = dict(zip(rhdr, r))
@@ -87,6 +114,13 @@ def report(path):
             rd, wr = dram[key]
             print(f"   dram__bytes_read.sum: {rd:.0f} B, dram__bytes_write.sum: {wr:.0f} B, "
                   f"traffic: {rd + wr:.0f} B")
+        if key in extra:
+            vals, stalls = extra[key]
+            if vals:
+                print("   pipes (% of peak, active): " + ", ".join(vals))
+            if stalls:
+                print("   top stalls (warps per issue): " +
+                      ", ".join(f"{n} {v:.2f}" for v, n in stalls))
         print()
 
 
