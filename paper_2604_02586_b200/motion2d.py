@@ -7,7 +7,6 @@ like the reference's list of ViewMotion but only builds the Python objects that 
 
 from __future__ import annotations
 
-import ctypes
 import enum
 from dataclasses import dataclass, field
 

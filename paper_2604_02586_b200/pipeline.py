@@ -24,7 +24,7 @@ import numpy as np
 from .config import Config
 from .core import Gaussian3D, cameras_array, gaussians_array
 from .errors import DimensionMismatch, InvalidConfig
-from .motion2d import Status, ViewAccumulators, ViewMotionList
+from .motion2d import ViewAccumulators
 from .multiview import MotionUpdateList
 
 
