@@ -1,7 +1,7 @@
 """Write profiles/k2_traffic_<cfg>.json (per-launch DRAM bytes and executed warp instructions of
 K2) from an `ncu --set full` report; bench.py reads it for roofline.traffic / issue_roofline.
 
-    python tools/k2_traffic.py REPORT.ncu-rep cfg2 "profiles/r02_kernels_cfg2.txt (...)"
+    python tools/k2_traffic.py REPORT.ncu-rep cfg2 "profiles/r02_kernels_cfg2.txt (...)" [OUTDIR]
 """
 
 import csv
@@ -31,8 +31,9 @@ def main():
                "executed_warp_instructions_per_launch":
                    int(float(d["smsp__inst_executed.sum"].replace(",", ""))),
                "source": source}
-        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                            "profiles", f"k2_traffic_{cfg}.json")
+        outdir = sys.argv[4] if len(sys.argv) > 4 else os.path.join(
+            os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+        path = os.path.join(outdir, f"k2_traffic_{cfg}.json")
         with open(path, "w") as f:
             json.dump(res, f)
         print(path, res)

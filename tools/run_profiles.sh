@@ -1,26 +1,42 @@
-# Round-2 measurement pass on one B200 (run under gpurun); outputs in gpurun_out/r02_*.
+# Round-2 measurement pass on one B200 (run under gpurun); outputs in gpurun_out/r02_* (text and
+# small files only: the ncu reports are summarised on the box and deleted, gpurun copies back at
+# most 64 MiB).
 #   bench lines (weak, every BASELINE config), the reference arm (cfg2), strong-scaling clips,
 #   ncu launch lists of whole frames (cfg2, cfg5) and --set full captures of one whole frame
 #   (cfg2, cfg5) plus K2 alone at cfg1/3/4 (roofline.traffic of every config).
 cd ${GRAFT_REPO_ROOT:-.}
-mkdir -p gpurun_out
-O=gpurun_out
-timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/r02_bench_reference_cfg2.json 2> $O/r02_bench_reference_cfg2.err
+mkdir -p gpurun_out/r02
+O=gpurun_out/r02
+STAGE=${STAGE:-all}
+if [ $STAGE = all -o $STAGE = bench ]; then
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_reference_cfg2.json 2> $O/bench_reference_cfg2.err
 for c in cfg2 cfg1 cfg3 cfg4 cfg5; do
   extra=""; [ $c != cfg2 ] && extra="--no-cpu"
-  timeout 900 python bench.py --config $c --steps 20 --warmup 5 $extra > $O/r02_bench_$c.json 2> $O/r02_bench_$c.err
+  timeout 900 python bench.py --config $c --steps 20 --warmup 5 $extra > $O/bench_$c.json 2> $O/bench_$c.err
 done
-timeout 900 python bench.py --config cfg5 --clip-frames 8 --steps 3 --warmup 1 > $O/r02_bench_cfg5_clip8.json 2> $O/r02_bench_cfg5_clip8.err
-timeout 900 python bench.py --config cfg4 --clip-frames 8 --steps 5 --warmup 2 > $O/r02_bench_cfg4_clip8.json 2> $O/r02_bench_cfg4_clip8.err
+timeout 900 python bench.py --config cfg5 --clip-frames 8 --steps 3 --warmup 1 > $O/bench_cfg5_clip8.json 2> $O/bench_cfg5_clip8.err
+timeout 900 python bench.py --config cfg4 --clip-frames 8 --steps 5 --warmup 2 > $O/bench_cfg4_clip8.json 2> $O/bench_cfg4_clip8.err
+fi
+if [ $STAGE = all -o $STAGE = ncu ]; then
 for c in cfg2 cfg5; do
   timeout 600 ncu --nvtx --nvtx-include "frame/" --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $O/r02_launches_$c.csv python tools/profile_frame.py --config $c --frames 3 > $O/r02_ncu_launch_$c.log 2>&1
-  # one whole frame (the third: launches 2F..3F-1 of the frame ranges)
-  timeout 1500 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "frame/" \
-    --launch-skip 70 --launch-count 35 -o $O/r02_frame_$c -f python tools/profile_frame.py --config $c --frames 3 > $O/r02_ncu_full_$c.log 2>&1
+    --log-file $O/launches_$c.csv python tools/profile_frame.py --config $c --frames 3 > $O/ncu_launch_$c.log 2>&1
+  python tools/summarize_ncu.py launches $O/launches_$c.csv > $O/launches_$c.txt 2>&1
+  # one whole frame (the third one)
+  timeout 1500 ncu --set full --clock-control none --nvtx --nvtx-include "frame/" \
+    --launch-skip 70 --launch-count 35 -o /tmp/frame_$c -f python tools/profile_frame.py --config $c --frames 3 > $O/ncu_full_$c.log 2>&1
+  python tools/summarize_ncu.py report /tmp/frame_$c.ncu-rep > $O/kernels_$c.txt 2>&1
+  python tools/k2_traffic.py /tmp/frame_$c.ncu-rep $c "profiles/r02_kernels_$c.txt (ncu --set full --clock-control none of one whole $c frame via tools/profile_frame.py)" $O >> $O/ncu_full_$c.log 2>&1
 done
 for c in cfg1 cfg3 cfg4; do
   timeout 900 ncu --set full --clock-control none -k regex:k2_raster --launch-skip 2 --launch-count 1 \
-    -o $O/r02_k2_$c -f python tools/profile_frame.py --config $c --frames 4 > $O/r02_ncu_k2_$c.log 2>&1
+    -o /tmp/k2_$c -f python tools/profile_frame.py --config $c --frames 4 > $O/ncu_k2_$c.log 2>&1
+  python tools/summarize_ncu.py report /tmp/k2_$c.ncu-rep > $O/k2_$c.txt 2>&1
+  python tools/k2_traffic.py /tmp/k2_$c.ncu-rep $c "profiles/r02_k2_$c.txt (ncu --set full --clock-control none of K2 at $c via tools/profile_frame.py)" $O >> $O/ncu_k2_$c.log 2>&1
 done
+# K2 alone at cfg2 with source lines (small report kept for the per-line attribution)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k2_raster --launch-skip 2 --launch-count 1 \
+  -o $O/k2_cfg2 -f python tools/profile_frame.py --config cfg2 --frames 4 > $O/ncu_k2_cfg2.log 2>&1
+fi
+du -sh $O
 echo done
