@@ -62,13 +62,17 @@ enum Stage { ST_PROJECT = 0, ST_DEPTH_SORT, ST_TILE_SORT, ST_RASTER, ST_SOLVE, S
 
 }  // namespace
 
+struct ByteToU32 {
+  __host__ __device__ uint32_t operator()(uint8_t x) const { return x; }
+};
+
 struct ts_plan {
   // binning state
   DevBuf cams, rec, dkey, dkey2, dval, dval2, depth64, ntiles, status, bbox, off_sorted,
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf k2_stats;
-  DevBuf partial, flag, touched, k3_list, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
+  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
       mot_sw;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
@@ -131,7 +135,8 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2, &p->knn_val,
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
                           &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
-                          &p->touched, &p->k3_list, &p->tie_runs, &p->tie_tmp};
+                          &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
+                          &p->tie_tmp};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -149,7 +154,8 @@ void release_all(ts_plan *p) {
                     &p->seg_end, &p->knn_part, &p->knn_grid, &p->knn_key, &p->knn_key2,
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
                     &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
-                    &p->touched, &p->k3_list, &p->tie_runs, &p->tie_tmp};
+                    &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
+                    &p->tie_tmp};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -610,6 +616,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (use_touched) {
     ENSURE(p->touched, NV + 8);
     ENSURE(p->k3_list, 4 * (NV + 8));
+    ENSURE(p->k3_rank, 4 * (NV + 8));
+    ENSURE(p->k3_fits, k3_fit_bytes() * (NV + 1));
   }
   cudaEvent_t e3 = p->mark_begin(s);
   TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
@@ -628,18 +636,26 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   // K3 and K4 stay separate: a fused per-Gaussian K3+K4 serialises the memory-bound per-view
   // fits inside a 200-register thread and measured 3.0 ms vs 0.6 + 1.5 ms (cfg2).
   cudaEvent_t e4 = p->mark_begin(s);
-  if (use_touched) {  // the touched gvs in gv order (the fits of K3), count on the device
+  if (use_touched) {  // the touched gvs in gv order (K3's fits), count on the device, ranks
     uint32_t *list = ptr<uint32_t>(p->k3_list), *n_list = list + NV + 4;
     TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
       return cub::DeviceSelect::Flagged(tmp, bytes, cub::CountingInputIterator<uint32_t>(0),
                                         ptr<uint8_t>(p->touched), list, n_list, (int)NV, s);
+    }));
+    cub::TransformInputIterator<uint32_t, ByteToU32, const uint8_t *> t_it(
+        ptr<uint8_t>(p->touched), ByteToU32{});
+    TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+      return cub::DeviceScan::ExclusiveSum(tmp, bytes, t_it, ptr<uint32_t>(p->k3_rank), (int)NV,
+                                           s);
     }));
   }
   launch_k3_solve(ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), ptr<uint32_t>(p->inst_base),
                   ptr<uint32_t>(p->ntiles), ptr<int16_t>(p->bbox), NV, p->cfg, m,
                   use_touched ? ptr<uint8_t>(p->touched) : nullptr,
                   use_touched ? ptr<uint32_t>(p->k3_list) : nullptr,
-                  use_touched ? ptr<uint32_t>(p->k3_list) + NV + 4 : nullptr, s);
+                  use_touched ? ptr<uint32_t>(p->k3_list) + NV + 4 : nullptr,
+                  use_touched ? ptr<uint32_t>(p->k3_rank) : nullptr,
+                  use_touched ? p->k3_fits.p : nullptr, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 

@@ -40,7 +40,9 @@ bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched 
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, const uint8_t *touched,
-                     const uint32_t *list, const uint32_t *n_list, cudaStream_t s);
+                     const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
+                     void *fits, cudaStream_t s);
+size_t k3_fit_bytes();  // per touched gv, the compact fit record of K3
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
                       int64_t n, double det_floor, int min_pixels, double min_weight,

@@ -101,23 +101,31 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve(const Partial 
 // K3 split by K2's per-gv "touched" bytes (a gv with at least one tracked contribution).  At the
 // large configs most gvs are occluded (cfg5: ~7% touched), and a warp with any touched lane
 // waited on the whole bbox -> slot base -> flags -> partials chain.  Instead:
-//   select (CUB DeviceSelect::Flagged, api.cu): the touched gvs, in gv order;
-//   k3_defaults: every untouched gv's motion = UNSOLVABLE / A = I / b = 0 / zero sums
-//                (coalesced streaming stores, no dependent loads);
-//   k3_solve_list: the fit of the listed gvs (one thread each, big bboxes per warp as k3_solve).
-// Every gv is written exactly once; results do not depend on the split.
-__global__ void __launch_bounds__(256) k3_defaults(const uint8_t *__restrict__ touched, int64_t NV,
-                                                   ts_motions m) {
+//   select + scan (CUB, api.cu): the touched gvs in gv order, and each gv's rank among them;
+//   k3_solve_list: the fits of the listed gvs, written to a compact array in list order
+//                  (coalesced: scattered 1-8 byte writes into the dense outputs made partial
+//                  sectors and read-modify-writes);
+//   k3_merge: every gv's dense motion -- its fit, or UNSOLVABLE / A = I / b = 0 / zero sums --
+//             with full coalesced stores.
+// Results do not depend on the split (tests compare against the oracle and across runs).
+__global__ void __launch_bounds__(256) k3_merge(const uint8_t *__restrict__ touched,
+                                                const uint32_t *__restrict__ rank,
+                                                const GvMotion *__restrict__ fits, int64_t NV,
+                                                ts_motions m) {
   const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gv >= NV || touched[gv]) return;
+  if (gv >= NV) return;
   GvMotion r;
-  r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
-  r.b[0] = 0.0; r.b[1] = 0.0;
-  r.wsum = 0.0;
-  r.static_wsum = 0.0;
-  r.count = 0;
-  r.static_count = 0;
-  r.status = TS_STATUS_UNSOLVABLE;
+  if (touched[gv]) {
+    r = fits[rank[gv]];
+  } else {
+    r.a[0] = 1.0; r.a[1] = 0.0; r.a[2] = 0.0; r.a[3] = 1.0;
+    r.b[0] = 0.0; r.b[1] = 0.0;
+    r.wsum = 0.0;
+    r.static_wsum = 0.0;
+    r.count = 0;
+    r.static_count = 0;
+    r.status = TS_STATUS_UNSOLVABLE;
+  }
   store_motion(m, gv, r);
 }
 
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
     const Partial *__restrict__ partial, const uint8_t *__restrict__ flag,
     const uint32_t *__restrict__ inst_base, const int16_t *__restrict__ bbox,
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ n_list, double det_floor,
-    int min_pixels, double min_weight, ts_motions m) {
+    int min_pixels, double min_weight, GvMotion *__restrict__ fits) {
   const int lane = threadIdx.x & 31;
   const uint32_t nl = *n_list;
   // grid-stride over the device-side count (the grid is sized for the SMs, not the worst case)
@@ -143,11 +151,8 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
     ax = ((int)bb.x + (int)bb.y) >> 1;
     ay = ((int)bb.z + (int)bb.w) >> 1;
   }
-  if (valid && !big) {
-    const GvMotion r = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels,
-                                min_weight);
-    store_motion(m, gv, r);
-  }
+  if (valid && !big)
+    fits[i] = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels, min_weight);
   uint32_t bigmask = __ballot_sync(0xffffffffu, valid && big);
   while (bigmask) {
     const int j = __ffs(bigmask) - 1;
@@ -167,8 +172,7 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
       scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
     }
     if (lane == j)
-      store_motion(m, gv, solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels,
-                                        min_weight));
+      fits[i] = solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
   }
   }
 }
@@ -266,10 +270,13 @@ __global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ se
 
 static inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+size_t k3_fit_bytes() { return sizeof(GvMotion); }
+
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, const uint8_t *touched,
-                     const uint32_t *list, const uint32_t *n_list, cudaStream_t s) {
+                     const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
+                     void *fits, cudaStream_t s) {
   if (!nv_total) return;
   if (!touched) {  // every gv walks its flags
     k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, bbox, nv_total,
@@ -277,13 +284,14 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
                                                    m);
     return;
   }
-  k3_defaults<<<blocks(nv_total, 256), 256, 0, s>>>(touched, nv_total, m);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(blocks(nv_total, 256), (int64_t)sms * 8);
+  GvMotion *f = reinterpret_cast<GvMotion *>(fits);
   k3_solve_list<<<(unsigned)grid, 256, 0, s>>>(partial, flag, inst_base, bbox, list, n_list,
-                                               cfg.det_floor, cfg.min_pixels, cfg.min_weight, m);
+                                               cfg.det_floor, cfg.min_pixels, cfg.min_weight, f);
+  k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank, f, nv_total, m);
 }
 
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
