@@ -18,7 +18,7 @@ timeout 900 python bench.py --config cfg5 --clip-frames 8 --steps 3 --warmup 1 >
 timeout 900 python bench.py --config cfg4 --clip-frames 8 --steps 5 --warmup 2 > $O/bench_cfg4_clip8.json 2> $O/bench_cfg4_clip8.err
 fi
 if [ $STAGE = all -o $STAGE = ncu ]; then
-for c in cfg2 cfg5; do
+for c in ${FRAME_CFGS:-cfg2 cfg5}; do
   timeout 600 ncu --nvtx --nvtx-include "frame/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches_$c.csv python tools/profile_frame.py --config $c --frames 3 > $O/ncu_launch_$c.log 2>&1
   python tools/summarize_ncu.py launches $O/launches_$c.csv > $O/launches_$c.txt 2>&1
@@ -28,15 +28,17 @@ for c in cfg2 cfg5; do
   python tools/summarize_ncu.py report /tmp/frame_$c.ncu-rep > $O/kernels_$c.txt 2>&1
   python tools/k2_traffic.py /tmp/frame_$c.ncu-rep $c "profiles/r02_kernels_$c.txt (ncu --set full --clock-control none of one whole $c frame via tools/profile_frame.py)" $O >> $O/ncu_full_$c.log 2>&1
 done
-for c in cfg1 cfg3 cfg4; do
-  timeout 900 ncu --set full --clock-control none -k regex:k2_raster --launch-skip 2 --launch-count 1 \
-    -o /tmp/k2_$c -f python tools/profile_frame.py --config $c --frames 4 > $O/ncu_k2_$c.log 2>&1
+for c in ${K2_CFGS:-cfg1 cfg3 cfg4}; do
+  # K2 of the second timed frame (NVTX "frame" ranges: the tracker's dominant-mode launches of
+  # the input generation are outside them)
+  timeout 900 ncu --set full --clock-control none --nvtx --nvtx-include "frame/" -k regex:k2_raster \
+    --launch-skip 1 --launch-count 1 -o /tmp/k2_$c -f python tools/profile_frame.py --config $c --frames 3 > $O/ncu_k2_$c.log 2>&1
   python tools/summarize_ncu.py report /tmp/k2_$c.ncu-rep > $O/k2_$c.txt 2>&1
   python tools/k2_traffic.py /tmp/k2_$c.ncu-rep $c "profiles/r02_k2_$c.txt (ncu --set full --clock-control none of K2 at $c via tools/profile_frame.py)" $O >> $O/ncu_k2_$c.log 2>&1
 done
 # K2 alone at cfg2 with source lines (small report kept for the per-line attribution)
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k2_raster --launch-skip 2 --launch-count 1 \
-  -o $O/k2_cfg2 -f python tools/profile_frame.py --config cfg2 --frames 4 > $O/ncu_k2_cfg2.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "frame/" -k regex:k2_raster \
+  --launch-skip 1 --launch-count 1 -o $O/k2_cfg2 -f python tools/profile_frame.py --config cfg2 --frames 3 > $O/ncu_k2_cfg2.log 2>&1
 fi
 du -sh $O
 echo done
