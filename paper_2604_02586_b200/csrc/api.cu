@@ -88,6 +88,8 @@ struct ts_plan {
   ts_config cfg{};
   bool timing = false;
   int k2_ctas_per_sm = 0;  // ts_plan_set_k2_ctas_per_sm (0: full residency)
+  int64_t k3_last_nv = 0;   // K3 split choice of the previous frame (see ts_frame_compensate)
+  bool k3_last_split = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks;
   size_t ev_next = 0;
@@ -611,8 +613,25 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
-  static const bool k3_split = !(getenv("TS_K3_SPLIT") && getenv("TS_K3_SPLIT")[0] == '0');
-  const bool use_touched = k3_split && k2_writes_touched();
+  // K3 split (touched-gv list + compact fits + merge) vs one thread per gv over all gvs: the
+  // split pays off when most gvs get no contribution (cfg5: 7% touched, K3 2.47 -> 1.27 ms),
+  // the single pass when many do (cfg2: ~40%, 0.44 vs 0.50 ms).  The plan keeps the touched
+  // fraction of its previous frame (copied back asynchronously; read after the next binning's
+  // stream synchronisation); the first frame splits from 16 M gvs on.  TS_K3_SPLIT=0/1 forces.
+  static const char *force = getenv("TS_K3_SPLIT");
+  bool split;
+  if (force && force[0]) {
+    split = force[0] != '0';
+  } else if (p->k3_last_nv == NV && p->k3_last_split) {
+    split = (double)p->host_small[8] < 0.25 * (double)NV;
+  } else if (p->k3_last_nv == NV) {
+    split = false;  // sticky: the single pass does not measure the touched fraction
+  } else {
+    split = NV >= (int64_t)16 << 20;
+  }
+  p->k3_last_nv = NV;
+  p->k3_last_split = split;
+  const bool use_touched = split && k2_writes_touched();
   if (use_touched) {
     ENSURE(p->touched, NV + 8);
     ENSURE(p->k3_list, 4 * (NV + 8));
@@ -656,6 +675,9 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                   use_touched ? ptr<uint32_t>(p->k3_list) + NV + 4 : nullptr,
                   use_touched ? ptr<uint32_t>(p->k3_rank) : nullptr,
                   use_touched ? p->k3_fits.p : nullptr, s);
+  if (use_touched)  // touched count for the next frame's choice
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 8, ptr<uint32_t>(p->k3_list) + NV + 4, 4,
+                                cudaMemcpyDeviceToHost, s));
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
 

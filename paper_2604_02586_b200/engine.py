@@ -549,8 +549,12 @@ class StreamingEngine:
         copy_ms = (g_host.numel() * g_host.element_size() + t_host.numel() *
                    t_host.element_size() + v_host.numel()) / (self.H2D_GBS * 1e6)
         if self._last_zero_copy:
-            # reading in place: copy the whole arrays when that copy hides under the period
-            want_zero_copy = not copy_ms < 0.85 * self._compute_ms
+            # reading in place: copy the whole arrays when copying steps were measured faster,
+            # or (never measured) when the estimated copy hides under the period
+            if self._copy_ms_meas is not None:
+                want_zero_copy = not self._copy_ms_meas < 0.97 * self._compute_ms
+            else:
+                want_zero_copy = not copy_ms < 0.85 * self._compute_ms
         else:
             # copying: go back once the copying steps are measured slower than in-place ones
             # (the copy sits in their period, so the in-place estimate is never refreshed here)

@@ -139,3 +139,14 @@ def test_copy_mode_returns_when_copies_are_slower():
     se._timing = [(_Ev(100.0 + 5.3 * k), _Ev(100.0 + 5.3 * k), 0, False) for k in range(8)]
     votes = StreamingEngine.SWITCH_VOTES
     assert _choose_n(se, 273.0, votes) == [False] * (votes - 1) + [True]
+
+
+def test_measured_copy_period_prevents_oscillation():
+    """Once copying steps were measured slower than reading in place, the optimistic estimate
+    (copy_ms < 0.85 period) no longer sends the stream back to copying."""
+    se = _engine(period_ms=4.0, steps=8)
+    se._copy_ms_meas = 4.3           # measured: copying steps took longer
+    assert _choose_n(se, 150.0, 6) == [True] * 6   # 3.0 ms estimate < 0.85 * 4.0, ignored
+    se._copy_ms_meas = 3.5           # measured faster: switch after the votes
+    votes = StreamingEngine.SWITCH_VOTES
+    assert _choose_n(se, 150.0, votes) == [True] * (votes - 1) + [False]
