@@ -417,14 +417,18 @@ def run_ours(args):
         return ms_, streamer.steps_zero_copy, streamer.steps_full_copy
 
     import gc
-    ms_e2e_copy = time_e2e(False)[0]
-    gc.collect()  # the previous streamer's second engine
-    torch.cuda.empty_cache()
-    ms_e2e_zc = time_e2e(True)[0]
-    gc.collect()
-    torch.cuda.empty_cache()
-    # the StreamingEngine default: per-step choice between the two
-    ms_e2e, n_zc, n_fc = time_e2e("auto")
+    if args.no_e2e:  # experiments only: the e2e keys are then absent from the line
+        ms_e2e_copy = ms_e2e_zc = ms_e2e = float("nan")
+        n_zc = n_fc = 0
+    else:
+        ms_e2e_copy = time_e2e(False)[0]
+        gc.collect()  # the previous streamer's second engine
+        torch.cuda.empty_cache()
+        ms_e2e_zc = time_e2e(True)[0]
+        gc.collect()
+        torch.cuda.empty_cache()
+        # the StreamingEngine default: per-step choice between the two
+        ms_e2e, n_zc, n_fc = time_e2e("auto")
     occupied = eng.occupied_tiles()
     track_px_bytes = 2 * t_hosts[0].element_size() + 1
     h2d_copy = g_host.numel() * 8 + t_hosts[0].numel() * t_hosts[0].element_size() + \
@@ -642,6 +646,7 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=1,
                     help="whole frames timed for the cpu_baseline of the GPU arm")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="experiments: skip the e2e runs")
     ap.add_argument("--clip-frames", type=int, default=0,
                     help="strong scaling: a step is a clip of this many target frames sharded "
                          "over the ranks, binned once per rank (0: weak scaling, one frame pair "
