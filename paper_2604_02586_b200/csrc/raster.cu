@@ -88,7 +88,6 @@ struct K2Warp {
   uint32_t slot[32], gvid[32];
   int2 anc[32];       // moment anchor (bbox centre pixel) of each record (accumulate mode)
   double w[K2_FLUSH][K2_WROW];
-  uint8_t plist[K2_FLUSH][64];  // per pending Gaussian: its contributing pixels, in pixel order
   TrackT trk_u[64], trk_v[64];  // track targets in their input precision
 };
 
@@ -143,16 +142,18 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
   double m[TS_NMOM];
 #pragma unroll
   for (int q = 0; q < TS_NMOM; q++) m[q] = 0.0;
-  // every lane of Gaussian kk: its whole count (no shuffle needed)
-  const uint32_t cnt = (uint32_t)__popcll(my_cm), scnt = (uint32_t)__popcll(my_cm & static64);
+  uint32_t cnt = 0, scnt = 0;
   if (my_cm) {
     const double ax = (double)my_ax, ay = (double)my_ay;
     const double bx = (double)(qx0 - my_ax), by = (double)(qy0 - my_ay);
     // the LPG lanes of Gaussian kk take every LPG-th of its contributing pixels (lane qq starts
-    // at the qq-th): balanced trip counts whatever the pixels' rows; the pixels come from the
-    // Gaussian's list (written when it became pending), not from bit scans of the mask
-    for (uint32_t r = qq; r < cnt; r += LPG) {
-      const int p = S.plist[kk][r];
+    // at the qq-th): balanced trip counts whatever the pixels' rows
+    uint64_t bits = my_cm;
+    for (int k = 0; k < qq; k++) bits &= bits - 1;
+    while (bits) {
+      const int p = __ffsll((long long)bits) - 1;
+#pragma unroll
+      for (int k = 0; k < LPG; k++) bits &= bits - 1;
       const double w = S.w[kk][p];
       const double dx = bx + (double)(p & 7), dy = by + (double)(p >> 3);
       const double ua = (double)S.trk_u[p] - ax, va = (double)S.trk_v[p] - ay;
@@ -171,12 +172,16 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
       m[11] += wy * va;
       const bool st = (static64 >> p) & 1ull;
       m[12] += st ? w : 0.0;
+      scnt += st;
+      cnt++;
     }
   }
 #pragma unroll
   for (int d = K2_FLUSH; d < 32; d <<= 1) {
 #pragma unroll
     for (int q = 0; q < TS_NMOM; q++) m[q] += __shfl_xor_sync(0xffffffffu, m[q], d);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
   }
   if (kk < kcount && cnt > 0 && qq < 4) {
     // the four lanes of a Gaussian hold identical sums: each stores a quarter of the record
@@ -203,7 +208,6 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
   for (int k = threadIdx.x; k < TS_EXP_TABLE; k += blockDim.x) etab[k] = exp(-k / 64.0);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t lt_mask = (1u << lane) - 1u;
   K2Warp<TrackT> &S =
       reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
   const uint32_t n_units = 4u * *P.n_items;
@@ -343,14 +347,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
             }
             if (cm0 | cm1) {  // Gaussians without a tracked contribution need no flush slot
               if (lane == 0 && P.touched) P.touched[S.gvid[j]] = 1;
-              if (k0) {
-                S.w[kpend][lane] = w0;
-                S.plist[kpend][__popc(cm0 & lt_mask)] = (uint8_t)lane;
-              }
-              if (k1) {
-                S.w[kpend][lane + 32] = w1;
-                S.plist[kpend][__popc(cm0) + __popc(cm1 & lt_mask)] = (uint8_t)(lane + 32);
-              }
+              if (k0) S.w[kpend][lane] = w0;
+              if (k1) S.w[kpend][lane + 32] = w1;
               if ((lane & (K2_FLUSH - 1)) == kpend) {  // this Gaussian's flush lanes
                 my_cm = (uint64_t)cm0 | ((uint64_t)cm1 << 32);
                 my_slot = S.slot[j];
