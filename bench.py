@@ -298,22 +298,11 @@ def run_ours(args):
 
     def step(k):
         i = k % n_fly
-        torch.cuda.set_device(local)  # also when run on an engine's issue thread
         if gather_bufs is not None and gather_ev[i] is not None:
             streams[i].wait_event(gather_ev[i])  # outs[i] was last read by a gather
         engs[i].bin(g_dev, cams, stream=streams[i])
         outs[i] = engs[i].compensate(tgt, val, outs[i], stream=streams[i])
         return i
-
-    # Each engine issues its frames from a thread of its own: ts_frame_bin synchronises its
-    # stream once (the instance count sizes the tile lists), and on one host thread that wait
-    # serialised the frames' binnings (the next frame's K1 was not even enqueued while the
-    # host waited).  ctypes releases the GIL in the C call, so the other engines' threads keep
-    # issuing.  Collectives stay on the main thread, in step order on every rank.
-    threaded = os.environ.get("TS_BENCH_THREADS", "1") != "0"
-    if threaded:
-        from concurrent.futures import ThreadPoolExecutor
-        execs = [ThreadPoolExecutor(max_workers=1) for _ in range(n_fly)]
 
     for s_ in streams:
         s_.wait_stream(stream)
@@ -321,14 +310,6 @@ def run_ours(args):
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
-
-    def issue_gather(i):
-        gather_stream.wait_stream(streams[i])
-        with torch.cuda.stream(gather_stream):
-            for t, buf in zip(update_tensors(outs[i]), gather_bufs):
-                dist.gather(t, buf if rank == 0 else None, dst=0)
-        gather_ev[i] = torch.cuda.Event()
-        gather_ev[i].record(gather_stream)
     if world > 1:
         # the updates of every rank's frame (delta mean, rotation, scale, status: 81 B per Gaussian)
         # are gathered to rank 0, which holds the frame-1 Gaussians they apply to.  Gathered
@@ -349,27 +330,19 @@ def run_ours(args):
         ev0.record(stream)
         for s_ in streams:
             s_.wait_stream(stream)
-        if threaded:
-            futs = {}
-            for k in range(args.steps):
-                if k >= n_fly:  # engine k % n_fly: its previous frame is issued; gather it
-                    i = futs.pop(k - n_fly).result()
-                    if world > 1:
-                        issue_gather(i)
-                futs[k] = execs[k % n_fly].submit(step, k)
-            for k in sorted(futs):
-                i = futs[k].result()
-                if world > 1:
-                    issue_gather(i)
-        else:
-            for k in range(args.steps):
-                # NVTX "step" ranges let ncu capture exactly the timed steps of this command:
-                #   ncu --nvtx --nvtx-include "step/" ... python bench.py
-                torch.cuda.nvtx.range_push("step")
-                i = step(k)
-                if world > 1:
-                    issue_gather(i)
-                torch.cuda.nvtx.range_pop()
+        for k in range(args.steps):
+            # NVTX "step" ranges let ncu capture exactly the timed steps of this command:
+            #   ncu --nvtx --nvtx-include "step/" ... python bench.py
+            torch.cuda.nvtx.range_push("step")
+            i = step(k)
+            if world > 1:
+                gather_stream.wait_stream(streams[i])
+                with torch.cuda.stream(gather_stream):
+                    for t, buf in zip(update_tensors(outs[i]), gather_bufs):
+                        dist.gather(t, buf if rank == 0 else None, dst=0)
+                gather_ev[i] = torch.cuda.Event()
+                gather_ev[i].record(gather_stream)
+            torch.cuda.nvtx.range_pop()
         for s_ in streams:
             stream.wait_stream(s_)
         if world > 1:
