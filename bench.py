@@ -493,7 +493,10 @@ def run_ours(args):
                 "peak": 4 * 148 * 1965e6, "unit": "warp-instructions/s",
                 "frac": k2_instr / (k2_ms / 1e3) / (4 * 148 * 1965e6),
                 "instructions_per_launch": k2_instr},
-            "stage_ms": stage_ms, "tallies": tallies,
+            "stage_ms": stage_ms,
+            # one frame alone on one stream (latency), vs ms_per_step with frames in flight
+            "frame_latency_ms": round(sum(stage_ms.values()), 4),
+            "tallies": tallies,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

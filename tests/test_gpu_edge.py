@@ -175,3 +175,14 @@ def test_long_depth_tie_runs_bit_exact():
     np.testing.assert_array_equal(rng_[:, 1] - rng_[:, 0], ref["tile_count"])
     idx = gd.tile_order_index(rng_)
     np.testing.assert_array_equal(b["inst_gv"][idx].astype(np.int64), ref["inst_gid"])
+
+
+def test_empty_frame(scene7):
+    """No Gaussians (the reference returns empty lists): every stage handles N = 0."""
+    from paper_2604_02586_b200.engine import FrameEngine
+    _, cams, target, valid = scene7
+    eng = FrameEngine().bin(np.zeros((0, 11)), cams)
+    out = eng.compensate(target.astype(np.float32), valid.astype(np.uint8))
+    torch.cuda.synchronize()
+    assert out.status.numel() == 0 and out.motion_status.numel() == 0
+    assert out.tallies() == {"solved": 0, "static": 0, "unsolvable": 0}

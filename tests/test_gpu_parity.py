@@ -199,7 +199,7 @@ def _update_stats(st, delta, rot, scale, ref_st, ref_delta, ref_rot, ref_scale, 
 
 
 def _check_updates(st, delta, rot, scale, ref_st, ref_delta, ref_rot, ref_scale, g,
-                   max_status_flip_frac=1e-3):
+                   max_status_flip_frac=1e-4):
     n = len(st)
     flips = np.flatnonzero(st != ref_st)
     assert len(flips) <= max(2, max_status_flip_frac * n), f"update status flips: {flips[:20]}"
