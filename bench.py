@@ -59,7 +59,14 @@ CONFIGS = {
 METRIC = "Gaussian-views/sec motion-fit"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
-LAUNCHES_PER_STEP = 33  # our kernels per frame incl. CUB passes (profiles/r01_launches_cfg2.txt: 66 per 2 frames)
+# our kernels per frame incl. CUB passes (profiles/r02_launches_cfg2.txt: 99 per 3 frames); the
+# K3 split (touched list + scan + compact fits + merge, chosen from 16 M gvs on: cfg5) adds 5
+LAUNCHES_PER_STEP = 33
+LAUNCHES_K3_SPLIT = 5
+
+
+def launches_per_step(n, nv):
+    return LAUNCHES_PER_STEP + (LAUNCHES_K3_SPLIT if n * nv >= (16 << 20) else 0)
 
 
 def log(*a):
@@ -497,7 +504,7 @@ def run_ours(args):
             # one frame alone on one stream (latency), vs ms_per_step with frames in flight
             "frame_latency_ms": round(sum(stage_ms.values()), 4),
             "tallies": tallies,
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step(n, nv) * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -601,7 +608,9 @@ def run_clip(args):
                 "config": cfg, "frames_per_s": T / (ms / 1e3),
                 "parallelism": f"frame-sharded x{world} (strong: {T} frames per step)",
                 "frames_per_rank": [len(frames_for_rank(targets, r, world)) for r in range(world)],
-                "gpu_launches": None, "clocks": clk.summary()}
+                # per step: one binning (20 launches) + per frame K2-K4 (13, +5 with the K3 split)
+                "gpu_launches": args.steps * (20 + len(mine) * (launches_per_step(n, nv) - 20)),
+                "clocks": clk.summary()}
     if world > 1:
         dist.destroy_process_group()
     return line
