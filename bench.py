@@ -608,8 +608,8 @@ def run_clip(args):
                 "config": cfg, "frames_per_s": T / (ms / 1e3),
                 "parallelism": f"frame-sharded x{world} (strong: {T} frames per step)",
                 "frames_per_rank": [len(frames_for_rank(targets, r, world)) for r in range(world)],
-                # per step: one binning (20 launches) + per frame K2-K4 (13, +5 with the K3 split)
-                "gpu_launches": args.steps * (20 + len(mine) * (launches_per_step(n, nv) - 20)),
+                # per step: one binning (21 launches) + per frame K2-K4 (12, +5 with the K3 split)
+                "gpu_launches": args.steps * (21 + len(mine) * (launches_per_step(n, nv) - 21)),
                 "clocks": clk.summary()}
     if world > 1:
         dist.destroy_process_group()
