@@ -425,7 +425,7 @@ def run_ours(args):
 
     import gc
     if args.no_e2e:  # experiments only: the e2e keys are then absent from the line
-        ms_e2e_copy = ms_e2e_zc = ms_e2e = float("nan")
+        ms_e2e_copy = ms_e2e_zc = ms_e2e = ms_e2e_rect = float("nan")
         n_zc = n_fc = 0
     else:
         ms_e2e_copy = time_e2e(False)[0]
@@ -434,15 +434,22 @@ def run_ours(args):
         ms_e2e_zc = time_e2e(True)[0]
         gc.collect()
         torch.cuda.empty_cache()
+        ms_e2e_rect = time_e2e("rect")[0]
+        gc.collect()
+        torch.cuda.empty_cache()
         # the StreamingEngine default: per-step choice between the two
         ms_e2e, n_zc, n_fc = time_e2e("auto")
     occupied = eng.occupied_tiles()
+    rects = eng.track_rects().astype(np.int64)
+    rect_px = int(np.sum(np.maximum(rects[:, 2] - rects[:, 0] + 1, 0) *
+                         np.maximum(rects[:, 3] - rects[:, 1] + 1, 0)))
     track_px_bytes = 2 * t_hosts[0].element_size() + 1
     h2d_copy = g_host.numel() * 8 + t_hosts[0].numel() * t_hosts[0].element_size() + \
         v_hosts[0].numel()
     # zero-copy: Gaussians + the 256 pixels of every occupied tile (edge tiles: upper bound)
     h2d_zc = g_host.numel() * 8 + occupied * 256 * track_px_bytes
     h2d = (n_zc * h2d_zc + n_fc * h2d_copy) / max(n_zc + n_fc, 1)  # the auto run's steps
+    h2d_rect = g_host.numel() * 8 + rect_px * track_px_bytes
     d2h = res_host.numel() * 8
 
     line = None
@@ -488,7 +495,10 @@ def run_ours(args):
                                   "ms_per_step": ms_e2e_zc, "h2d_bytes_per_step": int(h2d_zc)},
                     "full_copy": {"value": n * nv * world / (ms_e2e_copy / 1e3),
                                   "ms_per_step": ms_e2e_copy,
-                                  "h2d_bytes_per_step": int(h2d_copy)}},
+                                  "h2d_bytes_per_step": int(h2d_copy)},
+                    "rect_copy": {"value": n * nv * world / (ms_e2e_rect / 1e3),
+                                  "ms_per_step": ms_e2e_rect,
+                                  "h2d_bytes_per_step": int(h2d_rect)}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k2_raster_accumulate", "algorithmic_bytes": bk2,

@@ -151,6 +151,20 @@ int ts_frame_binning(const ts_plan *plan, ts_binning *out);
  * reads the 4 x 64 track pixels of each. */
 int ts_frame_occupied_tiles(const ts_plan *plan, int64_t *out);
 
+/* Per view, the pixel rectangle the next ts_frame_compensate reads from the track arrays (the
+ * 16x16 tiles touched by any binned bbox; inclusive x0 y0 x1 y1, x1 < x0 when the view has no
+ * binned Gaussian), into rects[4 * n_views].  Host-side, valid once ts_frame_bin has returned: a
+ * caller holding tracks in host memory can DMA just these rows (cudaMemcpy2DAsync) into a device
+ * array of the full (V, H, W) layout.  No reference counterpart (a transfer plan). */
+int ts_frame_track_rects(const ts_plan *plan, int32_t *rects);
+
+/* Asynchronous DMA of exactly those rectangles, per view, from host track arrays (pinned for the
+ * copy to overlap) into device arrays of the same (V, H, W[, 2]) layout, on `stream`: the copy
+ * engine moves the ~third of the pixels the frame needs (cfg2) while the SMs compute. */
+int ts_copy_track_rects(const ts_plan *plan, const void *host_target, int32_t track_dtype,
+                        const uint8_t *host_valid, void *dev_target, uint8_t *dev_valid,
+                        void *stream);
+
 /* ---- stage entry points (reference-typed API) ---- */
 
 /* rasterize_weights, splat.py:113-195, for one view.  Runs K1 + K2 in contribution-emitting

@@ -81,6 +81,7 @@ struct ts_plan {
   DevBuf knn_part, knn_grid, knn_key, knn_key2, knn_val, knn_val2, knn_sp, knn_lo, knn_hi,
       reg_static, reg_source, reg_euler, k4_ws, drange, k2_sched, tie_runs, tie_tmp;
   uint32_t *host_small = nullptr;  // pinned scratch for size read-backs
+  int32_t *host_rects = nullptr;   // per-view union of binned bboxes (x0 y0 x1 y1), after binning
   int64_t n = 0, n_inst = 0, n_slots = 0, emit_n = 0, n_deg = 0;
   int V = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0, tpv = 0;
   const double *gaussians = nullptr;
@@ -326,6 +327,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   if (cfg) p->cfg = *cfg;
   const int64_t NV = n * V;
   if (!p->host_small) TS_CUDA_TRY(cudaMallocHost(&p->host_small, 64));
+  if (!p->host_rects) TS_CUDA_TRY(cudaMallocHost(&p->host_rects, 16 * 64));
 
   ENSURE(p->cams, sizeof(ts_camera) * V);
   TS_CUDA_TRY(cudaMemcpyAsync(p->cams.p, cams, sizeof(ts_camera) * V, cudaMemcpyHostToDevice, s));
@@ -346,7 +348,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   ENSURE(p->counters, 64);
 
   cudaEvent_t e0 = p->mark_begin(s);
-  ENSURE(p->drange, 8 * 64);
+  ENSURE(p->drange, 4 * (K1_RECT_OFFSET + 4 * 64));
   // depth key: view bits + quantised depth (at most 2^26 levels), TS_K1_KEY_BITS in all
   const int dbits = std::min(26, TS_K1_KEY_BITS - bits_for((uint64_t)V));
   launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, dbits, ptr<RasterRec>(p->rec),
@@ -393,6 +395,8 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 1, ptr<uint32_t>(p->inst_base) + NV, 4,
                                 cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 2, p->tie_runs.p, 4, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaMemcpyAsync(p->host_rects, ptr<uint32_t>(p->drange) + K1_RECT_OFFSET,
+                                16 * V, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
     p->n_inst = (int64_t)p->host_small[0];
     p->n_slots = (int64_t)p->host_small[1];
@@ -520,6 +524,7 @@ int ts_plan_destroy(ts_plan *p) {
   release_all(p);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   if (p->host_small) cudaFreeHost(p->host_small);
+  if (p->host_rects) cudaFreeHost(p->host_rects);
   delete p;
   return TS_OK;
 }
@@ -688,6 +693,50 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                  p->k4_ws.p, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_FUSE, e5, s);
+  return TS_OK;
+}
+
+int ts_frame_track_rects(const ts_plan *p, int32_t *rects) {
+  if (!p || !rects || p->V < 1 || !p->host_rects) return TS_E_INVALID_ARGUMENT;
+  for (int v = 0; v < p->V; v++) {
+    const int32_t *r = p->host_rects + 4 * v;
+    int32_t *o = rects + 4 * v;
+    if (p->n == 0 || r[2] < 0) {  // no binned Gaussian in this view: nothing is read
+      o[0] = o[1] = 0;
+      o[2] = o[3] = -1;
+      continue;
+    }
+    // K2 reads whole 8x8 quadrants of every touched 16x16 tile
+    o[0] = (r[0] / TS_TILE) * TS_TILE;
+    o[1] = (r[1] / TS_TILE) * TS_TILE;
+    o[2] = std::min(((r[2] / TS_TILE) + 1) * TS_TILE, p->W) - 1;
+    o[3] = std::min(((r[3] / TS_TILE) + 1) * TS_TILE, p->H) - 1;
+  }
+  return TS_OK;
+}
+
+int ts_copy_track_rects(const ts_plan *p, const void *host_target, int32_t track_dtype,
+                        const uint8_t *host_valid, void *dev_target, uint8_t *dev_valid,
+                        void *stream) {
+  if (!p || !host_target || !host_valid || !dev_target || !dev_valid) return TS_E_INVALID_ARGUMENT;
+  if (track_dtype != TS_TRACK_F32 && track_dtype != TS_TRACK_F64) return TS_E_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int32_t> r(4 * (size_t)p->V);
+  int rc = ts_frame_track_rects(p, r.data());
+  if (rc) return rc;
+  const size_t px = track_dtype == TS_TRACK_F32 ? 8 : 16;  // bytes per target pixel (u, v)
+  const size_t W = (size_t)p->W, H = (size_t)p->H;
+  for (int v = 0; v < p->V; v++) {
+    const int x0 = r[4 * v], y0 = r[4 * v + 1], x1 = r[4 * v + 2], y1 = r[4 * v + 3];
+    if (x1 < x0 || y1 < y0) continue;
+    const size_t off = ((size_t)v * H + (size_t)y0) * W + (size_t)x0;
+    const size_t w = (size_t)(x1 - x0 + 1), h = (size_t)(y1 - y0 + 1);
+    TS_CUDA_TRY(cudaMemcpy2DAsync(static_cast<char *>(dev_target) + off * px, W * px,
+                                  static_cast<const char *>(host_target) + off * px, W * px,
+                                  w * px, h, cudaMemcpyHostToDevice, s));
+    TS_CUDA_TRY(cudaMemcpy2DAsync(dev_valid + off, W, host_valid + off, W, w, h,
+                                  cudaMemcpyHostToDevice, s));
+  }
   return TS_OK;
 }
 

@@ -67,26 +67,51 @@ __global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, 
 
 // Per-view range of the binned depths (float bits, widened by directed rounding so that every
 // double depth lies inside; depth > 1e-6 > 0, so positive-float bit order is numeric order).
+// Also the per-view union of the binned bboxes (x0, y0, x1, y1 at drange + K1_RECT_OFFSET): the
+// pixels K2 can read lie in the tiles it touches -- the region a host-resident track array must
+// provide on the device (ts_frame_track_rects).
 __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__ depth64,
+                                                      const int8_t *__restrict__ status,
+                                                      const int16_t *__restrict__ bbox,
                                                       int64_t n, uint32_t *__restrict__ drange) {
   const int v = blockIdx.y;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  int rx0 = 0x7FFFFFFF, ry0 = 0x7FFFFFFF, rx1 = -1, ry1 = -1;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const double d = depth64[(int64_t)v * n + g];
+    const int64_t gv = (int64_t)v * n + g;
+    const double d = depth64[gv];
     if (d > 0.0) {
       lo = min(lo, __float_as_uint(__double2float_rd(d)));
       hi = max(hi, __float_as_uint(__double2float_ru(d)));
+    }
+    if (status[gv] == 3) {
+      const short4 b = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
+      rx0 = min(rx0, (int)b.x);
+      rx1 = max(rx1, (int)b.y);
+      ry0 = min(ry0, (int)b.z);
+      ry1 = max(ry1, (int)b.w);
     }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+    rx0 = min(rx0, __shfl_xor_sync(0xffffffffu, rx0, d));
+    ry0 = min(ry0, __shfl_xor_sync(0xffffffffu, ry0, d));
+    rx1 = max(rx1, __shfl_xor_sync(0xffffffffu, rx1, d));
+    ry1 = max(ry1, __shfl_xor_sync(0xffffffffu, ry1, d));
   }
   if ((threadIdx.x & 31) == 0) {
     if (lo != 0xFFFFFFFFu) atomicMin(&drange[2 * v], lo);
     if (hi != 0u) atomicMax(&drange[2 * v + 1], hi);
+    if (rx1 >= 0) {
+      int *r = reinterpret_cast<int *>(drange + K1_RECT_OFFSET) + 4 * v;
+      atomicMin(r, rx0);
+      atomicMin(r + 1, ry0);
+      atomicMax(r + 2, rx1);
+      atomicMax(r + 3, ry1);
+    }
   }
 }
 
@@ -273,6 +298,9 @@ __global__ void k1_range_init(uint32_t *drange, int V) {
   if (i < V) {
     drange[2 * i] = 0xFFFFFFFFu;
     drange[2 * i + 1] = 0u;
+    int *r = reinterpret_cast<int *>(drange + K1_RECT_OFFSET) + 4 * i;
+    r[0] = r[1] = 0x7FFFFFFF;
+    r[2] = r[3] = -1;
   }
 }
 
@@ -284,7 +312,7 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
   k1_range_init<<<1, 64, 0, s>>>(drange, V);
   k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, drange, dval,
                                                                   depth64, ntiles, status, bbox);
-  k1_depth_range<<<dim3(16, V), 256, 0, s>>>(depth64, n, drange);
+  k1_depth_range<<<dim3(16, V), 256, 0, s>>>(depth64, status, bbox, n, drange);
   k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dbits, dkey);
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,

@@ -7,6 +7,7 @@ namespace ts {
 
 enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
 
+constexpr int K1_RECT_OFFSET = 128;  // u32 offset of the per-view bbox unions in the drange buffer
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, int dbits,
                        RasterRec *rec, uint32_t *drange, uint32_t *dkey, uint32_t *dval,
                        double *depth64, uint32_t *ntiles, int8_t *status, int16_t *bbox,

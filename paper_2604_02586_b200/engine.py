@@ -177,6 +177,24 @@ class FrameEngine:
                     status=grab(b.gv_status, nv, np.int8),
                     bbox=grab(b.gv_bbox, nv, np.int16, 4))
 
+    def track_rects(self):
+        """(V, 4) int32 inclusive pixel rectangles (x0, y0, x1, y1) the next compensate reads."""
+        if self.grouped:
+            raise NotImplementedError("track_rects() of a grouped (multi-plan) camera rig")
+        r = np.empty((self.n_views, 4), np.int32)
+        nat.check(self._lib.ts_frame_track_rects(self.plan.handle, r.ctypes.data), "track_rects")
+        return r
+
+    def copy_track_rects(self, t_host, v_host, t_dev, v_dev, stream=None):
+        """DMA the track rectangles of the current binning from pinned host tensors into device
+        tensors of the same layout, on `stream` (asynchronous)."""
+        torch = _torch()
+        dtype = nat.TS_TRACK_F32 if t_host.dtype == torch.float32 else nat.TS_TRACK_F64
+        nat.check(self._lib.ts_copy_track_rects(self.plan.handle, t_host.data_ptr(), dtype,
+                                                v_host.data_ptr(), t_dev.data_ptr(),
+                                                v_dev.data_ptr(), nat.stream_ptr(stream)),
+                  "copy_track_rects")
+
     def occupied_tiles(self):
         """Non-empty (view, tile) lists of the current binning (K2 reads 256 track pixels each)."""
         total = 0
@@ -402,8 +420,9 @@ class StreamingEngine:
         self._last_zero_copy = True
         self._votes = 0
         self._burst = 0
-        self.steps_zero_copy = 0  # steps whose tracks were read in place / copied whole
-        self.steps_full_copy = 0
+        self.steps_zero_copy = 0  # steps whose tracks were read in place / copied whole /
+        self.steps_full_copy = 0  # copied as the tiles the frame reads ("rect")
+        self.steps_rect_copy = 0
         self._timing = []  # (start, end) events of computed steps not yet read
         self.engines = [engine if engine is not None else FrameEngine()] + \
             [FrameEngine() for _ in range(self.N_ENGINES - 1)]
@@ -455,7 +474,7 @@ class StreamingEngine:
 
     def _compute(self, pending):
         torch = _torch()
-        i, g_d, t_d, v_d, ready, cameras, res_host, config = pending
+        i, g_d, t_d, v_d, ready, cameras, res_host, config, src = pending
         e = self._c % self.N_ENGINES
         self._c += 1
         eng, cs = self.engines[e], self.comp_streams[e]
@@ -463,6 +482,13 @@ class StreamingEngine:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(cs)
         eng.bin(g_d, cameras, config, stream=cs)
+        if src is not None:
+            # "rect": the binning is known, so only the tiles K2 will read are DMA'd (the copy
+            # engine works while the SMs run the other frames in flight)
+            eng.copy_track_rects(src[0], src[1], t_d, v_d, self.copy_stream)
+            copied = torch.cuda.Event()
+            copied.record(self.copy_stream)
+            cs.wait_event(copied)
         # the binning does not touch the outputs: only K2-K4 wait for their previous D2H
         if self._out_free[e] is not None:
             cs.wait_event(self._out_free[e])
@@ -499,9 +525,12 @@ class StreamingEngine:
         torch = _torch()
         i = self._k % self.N_SLOTS
         self._k += 1
-        zero_copy = self._choose_zero_copy(g_host, t_host, v_host) and \
+        rect = self.zero_copy_tracks == "rect" and _pinned_pair(t_host, v_host)
+        zero_copy = not rect and self._choose_zero_copy(g_host, t_host, v_host) and \
             _pinned_pair(t_host, v_host)
-        if zero_copy:
+        if rect:
+            self.steps_rect_copy += 1
+        elif zero_copy:
             self.steps_zero_copy += 1
         else:
             self.steps_full_copy += 1
@@ -514,12 +543,14 @@ class StreamingEngine:
             g_d.copy_(g_host, non_blocking=True)
             if zero_copy:
                 t_d, v_d = t_host, v_host  # read in place by K2
-            else:
+            elif not rect:
                 t_d.copy_(t_host, non_blocking=True)
                 v_d.copy_(v_host, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self.copy_stream)
-        prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config)
+        src = (t_host, v_host) if rect else None  # rectangles copied after the binning
+        prev, self._pending = self._pending, (i, g_d, t_d, v_d, ready, cameras, res_host, config,
+                                              src)
         return self._compute(prev) if prev is not None else None
 
     def _choose_zero_copy(self, g_host, t_host, v_host):

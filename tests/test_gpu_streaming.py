@@ -19,7 +19,7 @@ def _direct_rows(direct, g, cams, t, v):
                       o.status.to(torch.float64)[:, None]], 1).cpu()
 
 
-@pytest.mark.parametrize("zero_copy", [True, False, "auto"])
+@pytest.mark.parametrize("zero_copy", [True, False, "auto", "rect"])
 def test_streaming_matches_direct(zero_copy):
     """2 * N_SLOTS + 1 steps with distinct inputs: every input slot and every engine's outputs are
     reused; each step's result host buffer is reused too (read back before the next reuse).  In
@@ -157,3 +157,32 @@ def test_zero_copy_tracks_bit_identical(dtype):
         ctypes.c_void_p(v.ctypes.data), ctypes.byref(m), ctypes.byref(u), None)
     assert rc == nat.TS_E_INVALID_ARGUMENT
     assert eng.occupied_tiles() > 0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_track_rects_cover_every_read(dtype):
+    """ts_copy_track_rects DMAs only the tiles the binning touches into device arrays that are
+    otherwise garbage (NaN targets, invalid flags): the results equal the full-array run bit for
+    bit, so K2 never reads outside the rectangles."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_02586_b200.engine import FrameEngine
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    t = np.ascontiguousarray(target.astype(dtype))
+    v = np.ascontiguousarray(valid.astype(np.uint8))
+    eng = FrameEngine().bin(d["gaussians"], d["cameras"])
+    ref = eng.compensate(torch.from_numpy(t).cuda(), torch.from_numpy(v).cuda())
+    rects = eng.track_rects()
+    assert rects.shape == (len(d["cameras"]), 4)
+    area = ((rects[:, 2] - rects[:, 0] + 1) * (rects[:, 3] - rects[:, 1] + 1)).sum()
+    assert 0 < area < t.shape[0] * t.shape[1] * t.shape[2]
+    td = torch.full(t.shape, float("nan"), dtype=torch.from_numpy(t).dtype, device="cuda")
+    vd = torch.full(v.shape, 7, dtype=torch.uint8, device="cuda")
+    th, vh = torch.from_numpy(t).pin_memory(), torch.from_numpy(v).pin_memory()
+    eng.copy_track_rects(th, vh, td, vd)
+    got = eng.compensate(td, vd)
+    torch.cuda.synchronize()
+    for k in ("delta_mean", "rotation", "scale", "status", "motion_status", "motion_a",
+              "motion_b", "weight_sum", "pixel_count", "static_pixel_count"):
+        assert torch.equal(getattr(got, k), getattr(ref, k)), k
