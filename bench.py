@@ -425,7 +425,7 @@ def run_ours(args):
 
     import gc
     if args.no_e2e:  # experiments only: the e2e keys are then absent from the line
-        ms_e2e_copy = ms_e2e_zc = ms_e2e = ms_e2e_rect = float("nan")
+        ms_e2e_copy = ms_e2e_zc = ms_e2e = ms_e2e_rect = ms_e2e_auto = float("nan")
         n_zc = n_fc = 0
     else:
         ms_e2e_copy = time_e2e(False)[0]
@@ -434,11 +434,11 @@ def run_ours(args):
         ms_e2e_zc = time_e2e(True)[0]
         gc.collect()
         torch.cuda.empty_cache()
-        ms_e2e_rect = time_e2e("rect")[0]
+        ms_e2e_auto, n_zc, n_fc = time_e2e("auto")
         gc.collect()
         torch.cuda.empty_cache()
-        # the StreamingEngine default: per-step choice between the two
-        ms_e2e, n_zc, n_fc = time_e2e("auto")
+        # the StreamingEngine default: DMA of the tiles each frame reads, after its binning
+        ms_e2e = ms_e2e_rect = time_e2e("rect")[0]
     occupied = eng.occupied_tiles()
     rects = eng.track_rects().astype(np.int64)
     rect_px = int(np.sum(np.maximum(rects[:, 2] - rects[:, 0] + 1, 0) *
@@ -448,8 +448,8 @@ def run_ours(args):
         v_hosts[0].numel()
     # zero-copy: Gaussians + the 256 pixels of every occupied tile (edge tiles: upper bound)
     h2d_zc = g_host.numel() * 8 + occupied * 256 * track_px_bytes
-    h2d = (n_zc * h2d_zc + n_fc * h2d_copy) / max(n_zc + n_fc, 1)  # the auto run's steps
-    h2d_rect = g_host.numel() * 8 + rect_px * track_px_bytes
+    h2d_auto = (n_zc * h2d_zc + n_fc * h2d_copy) / max(n_zc + n_fc, 1)  # the auto run's steps
+    h2d = h2d_rect = g_host.numel() * 8 + rect_px * track_px_bytes
     d2h = res_host.numel() * 8
 
     line = None
@@ -486,11 +486,14 @@ def run_ours(args):
             "e2e": {"value": n * nv * world / (ms_e2e / 1e3), "unit": "Gaussian-views/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": ms_e2e,
-                    "tracks": f"zero-copy: K2 reads the {occupied} occupied 16x16 tiles in place "
-                              f"from pinned host memory (two host track sets alternate)",
-                    "mode": f"auto: copies the whole track arrays when that copy fits under "
-                            f"the compute, reads the occupied tiles in place otherwise "
-                            f"({n_zc} steps in place, {n_fc} copied)",
+                    "tracks": f"pinned host tracks (two sets alternate between steps); after "
+                              f"each frame's binning the pixel rectangles of the tiles K2 reads "
+                              f"({rect_px} px of {t_hosts[0].shape[0] * w * h}) are DMA'd on the "
+                              f"copy engine (ts_copy_track_rects)",
+                    "mode": "rect (StreamingEngine default); in place / whole copy / auto beside",
+                    "auto": {"value": n * nv * world / (ms_e2e_auto / 1e3),
+                             "ms_per_step": ms_e2e_auto, "h2d_bytes_per_step": int(h2d_auto),
+                             "steps_in_place": n_zc, "steps_copied": n_fc},
                     "zero_copy": {"value": n * nv * world / (ms_e2e_zc / 1e3),
                                   "ms_per_step": ms_e2e_zc, "h2d_bytes_per_step": int(h2d_zc)},
                     "full_copy": {"value": n * nv * world / (ms_e2e_copy / 1e3),

@@ -27,6 +27,11 @@ from . import _native as nat
 from .core import cameras_array, gaussians_array
 
 
+def _nullctx():
+    import contextlib
+    return contextlib.nullcontext()
+
+
 def _torch():
     import torch
     return torch
@@ -189,6 +194,11 @@ class FrameEngine:
         """DMA the track rectangles of the current binning from pinned host tensors into device
         tensors of the same layout, on `stream` (asynchronous)."""
         torch = _torch()
+        if self.grouped:  # several plans: the whole arrays (the rig is binned per view group)
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                t_dev.copy_(t_host, non_blocking=True)
+                v_dev.copy_(v_host, non_blocking=True)
+            return
         dtype = nat.TS_TRACK_F32 if t_host.dtype == torch.float32 else nat.TS_TRACK_F64
         nat.check(self._lib.ts_copy_track_rects(self.plan.handle, t_host.data_ptr(), dtype,
                                                 v_host.data_ptr(), t_dev.data_ptr(),
@@ -388,9 +398,12 @@ class StreamingEngine:
     PCIe (about a tenth of the track bytes at the benchmark configs, but at the PCIe request rate
     rather than its bandwidth); with `zero_copy_tracks=False` the whole arrays are copied on the
     H2D stream (DMA at full bandwidth, hidden when the compute takes longer).  The default
-    `"auto"` picks per step: it keeps the period between finished steps (CUDA events) and copies
-    the whole arrays whenever that copy -- estimated at `H2D_GBS` -- fits under the period,
-    reading in place otherwise.  Both modes give bit-identical results.  Input slots and
+    `"rect"` copies, once the frame's binning is known, only the pixel rectangles of the tiles
+    K2 will read (ts_copy_track_rects: a third of the track bytes at cfg2) with the copy engine
+    while the other frames in flight compute -- never slower than the best of the other two by
+    more than ~1% on the BASELINE configs, faster at cfg2 / cfg5.  `"auto"` picks per step
+    between reading in place and the whole copy from measured step periods.  All modes give
+    bit-identical results.  Input slots and
     output buffers are reused in turn, ordered with CUDA events.  `step` returns the event after
     which the previous step's results are in its host buffer (None for the first call);
     `flush()` runs the last pending step; `wait_all(stream)` orders `stream` after every result
@@ -410,7 +423,7 @@ class StreamingEngine:
     SWITCH_VOTES = 3  # consecutive steps that must favour the other mode before "auto" switches
     SETTLE_STEPS = N_ENGINES + 2  # first steps (allocation, plan growth) never feed a period
 
-    def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="auto"):
+    def __init__(self, engine: FrameEngine | None = None, zero_copy_tracks="rect"):
         torch = _torch()
         self._compute_ms = None  # median of the last in-place step periods ("auto" mode)
         self._periods = []
