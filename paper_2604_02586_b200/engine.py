@@ -445,6 +445,7 @@ class StreamingEngine:
             e_.plan.set_k2_ctas_per_sm(self.K2_CTAS_PER_SM)
         self.zero_copy_tracks = zero_copy_tracks
         self.copy_stream = torch.cuda.Stream()
+        self.rect_stream = torch.cuda.Stream()
         self.comp_streams = [torch.cuda.Stream() for _ in range(self.N_ENGINES)]
         self.d2h_stream = torch.cuda.Stream()
         self._slots = [None] * self.N_SLOTS
@@ -497,10 +498,14 @@ class StreamingEngine:
         eng.bin(g_d, cameras, config, stream=cs)
         if src is not None:
             # "rect": the binning is known, so only the tiles K2 will read are DMA'd (the copy
-            # engine works while the SMs run the other frames in flight)
-            eng.copy_track_rects(src[0], src[1], t_d, v_d, self.copy_stream)
+            # engine works while the SMs run the other frames in flight).  A stream of its own:
+            # on the input stream the copy would queue behind the next step's Gaussian copy,
+            # which nothing waits for yet; `ready` (this slot's Gaussians) already ordered it
+            # after the slot's previous use.
+            self.rect_stream.wait_event(ready)
+            eng.copy_track_rects(src[0], src[1], t_d, v_d, self.rect_stream)
             copied = torch.cuda.Event()
-            copied.record(self.copy_stream)
+            copied.record(self.rect_stream)
             cs.wait_event(copied)
         # the binning does not touch the outputs: only K2-K4 wait for their previous D2H
         if self._out_free[e] is not None:
