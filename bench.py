@@ -568,8 +568,14 @@ def run_clip(args):
                            outs[mine[0]].scale, outs[mine[0]].status)] for _ in range(slots)]
     gathered = [None] * slots
 
+    use_cache = not args.no_cache
+
     def step():
         eng.bin(g_dev, cams)  # once per clip step, shared by this rank's frames
+        if use_cache:
+            # the rank's frames share frame 0's contributions: rasterize once per clip
+            # (pipeline.py:191-196) and apply each frame's tracks to the cache
+            eng.build_cache()
         for j in range(slots):
             if j < len(mine):
                 if gathered[j] is not None:
@@ -612,7 +618,10 @@ def run_clip(args):
     if rank == 0:
         cfg = config_dict(args.config, scene)
         cfg["target_frame"] = f"clip of {T} target frames (frame 0 -> {targets[0]}..{targets[-1]})"
-        cfg["step"] = (f"one clip: K1 binning once per rank, then K2-K4 for each of the rank's "
+        cfg["step"] = (f"one clip: K1 binning and the contribution cache (K2 without tracks) "
+                       f"once per rank, then K2+K3 from the cache and K4 for each of the rank's "
+                       f"target frames; {T} frames over {world} GPU(s)" if use_cache else
+                       f"one clip: K1 binning once per rank, then K2-K4 for each of the rank's "
                        f"target frames; {T} frames over {world} GPU(s)")
         line = {"metric": METRIC, "value": T * n * nv / (ms / 1e3), "unit": "Gaussian-views/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -672,6 +681,8 @@ def main():
                     help="whole frames timed for the cpu_baseline of the GPU arm")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="experiments: skip the e2e runs")
+    ap.add_argument("--no-cache", action="store_true",
+                    help="clip mode: rasterize every target frame (no contribution cache)")
     ap.add_argument("--clip-frames", type=int, default=0,
                     help="strong scaling: a step is a clip of this many target frames sharded "
                          "over the ranks, binned once per rank (0: weak scaling, one frame pair "

@@ -72,7 +72,7 @@ struct ts_plan {
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf k2_stats;
-  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
+  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, cache_pool, cache_cursor, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
       mot_sw;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
@@ -90,6 +90,9 @@ struct ts_plan {
   bool timing = false;
   int k2_ctas_per_sm = 0;  // ts_plan_set_k2_ctas_per_sm (0: full residency)
   int64_t k3_last_nv = 0;   // K3 split choice of the previous frame (see ts_frame_compensate)
+  bool cache_valid = false;  // clip contribution cache (ts_frame_cache) of the current binning
+  uint64_t cache_cap = 0;    // pool capacity in doubles
+  uint64_t cache_used = 0;   // doubles handed out by the last build
   bool k3_last_split = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks;
@@ -139,7 +142,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
                           &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                           &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                          &p->tie_tmp};
+                          &p->tie_tmp, &p->cache_pool, &p->cache_cursor};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -158,7 +161,7 @@ void release_all(ts_plan *p) {
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
                     &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                     &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                    &p->tie_tmp};
+                    &p->tie_tmp, &p->cache_pool, &p->cache_cursor};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -315,6 +318,7 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
   if (rc) return rc;
   if (V > 64) return TS_E_INVALID_ARGUMENT;  // 6 view bits in the 32-bit depth key
   if (n < 0 || (uint64_t)n * (uint64_t)V >= 0xFFFFFFFFull) return TS_E_INVALID_ARGUMENT;
+  p->cache_valid = false;  // a new binning invalidates the clip's contribution cache
   p->n = n;
   p->V = V;
   p->W = cams[0].width;
@@ -617,6 +621,20 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.weight_sum) m.weight_sum = im.weight_sum;
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
+  if (p->cache_valid) {
+    // the clip's contribution cache: K2 + K3 as one pass over the cached contributions with
+    // this frame's tracks (no rasterization), then K4
+    cudaEvent_t e3 = p->mark_begin(s);
+    p->mark_end(ST_RASTER, e3, s);
+    cudaEvent_t e4 = p->mark_begin(s);
+    uint32_t *list = ptr<uint32_t>(p->k3_list);
+    launch_k23_cached(p->partial.p, ptr<double>(p->cache_pool), ptr<uint8_t>(p->flag),
+                      ptr<uint32_t>(p->inst_base), ptr<int16_t>(p->bbox), list, list + NV + 4, n,
+                      NV, p->W, p->H, track_target, track_dtype, track_valid, p->cfg, m,
+                      ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, s);
+    TS_CUDA_TRY(cudaGetLastError());
+    p->mark_end(ST_SOLVE, e4, s);
+  } else {
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
   // K3 split (touched-gv list + compact fits + merge) vs one thread per gv over all gvs: the
   // split pays off when most gvs get no contribution (cfg5: 7% touched, K3 2.47 -> 1.27 ms),
@@ -685,6 +703,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                                 cudaMemcpyDeviceToHost, s));
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_SOLVE, e4, s);
+  }
 
   if (!updates) return TS_OK;  // K2 + K3 only: the caller fuses (ts_update_all) over more views
   ENSURE(p->k4_ws, k4_workspace_bytes(n));
@@ -693,6 +712,68 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                  p->k4_ws.p, s);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_FUSE, e5, s);
+  return TS_OK;
+}
+
+int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
+  if (!p) return TS_E_INVALID_ARGUMENT;
+  if (!enable) {
+    p->cache_valid = false;
+    return TS_OK;
+  }
+  if (p->V < 1) return TS_E_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = p->n, NV = n * p->V, ns = p->n_slots;
+  ENSURE(p->partial, sizeof(Partial) * (ns + 1));
+  ENSURE(p->flag, ns + 8);
+  ENSURE(p->touched, NV + 8);
+  ENSURE(p->k3_list, 4 * (NV + 8));
+  ENSURE(p->k3_rank, 4 * (NV + 8));
+  ENSURE(p->k3_fits, k3_fit_bytes() * (NV + 1));
+  ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
+  ENSURE(p->cache_cursor, 8);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // every K2 warp may leave most of one chunk unused
+  const uint64_t slack = (uint64_t)sms * 8 * 4 * K2_CACHE_CHUNK;
+  if (p->cache_cap == 0) p->cache_cap = (uint64_t)std::max<int64_t>(8 * ns, 1 << 22) + slack;
+  for (int attempt = 0; attempt < 3; attempt++) {
+    ENSURE(p->cache_pool, 8 * p->cache_cap);
+    TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
+    TS_CUDA_TRY(cudaMemsetAsync(p->touched.p, 0, NV + 8, s));
+    TS_CUDA_TRY(cudaMemsetAsync(p->cache_cursor.p, 0, 8, s));
+    TS_CUDA_TRY(launch_k2(K2_CACHE, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
+                          ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
+                          ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0,
+                          p->tpv * p->V, nullptr, nullptr, p->W, p->H, p->tiles_x, p->tpv,
+                          p->cfg, ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0,
+                          nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                          p->k2_sched.p, s, p->k2_ctas_per_sm, ptr<uint8_t>(p->touched),
+                          ptr<double>(p->cache_pool),
+                          ptr<unsigned long long>(p->cache_cursor), p->cache_cap));
+    uint64_t used = 0;
+    TS_CUDA_TRY(cudaMemcpyAsync(&used, p->cache_cursor.p, 8, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (used <= p->cache_cap) {
+      p->cache_used = used;
+      break;
+    }
+    p->cache_cap = used + used / 8 + slack;  // pool too small: grow and rebuild
+    if (attempt == 2) return TS_E_CAPACITY;
+  }
+  // the touched gvs (any cached contribution) and their ranks: fixed for the clip
+  uint32_t *list = ptr<uint32_t>(p->k3_list), *n_list = list + NV + 4;
+  TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+    return cub::DeviceSelect::Flagged(tmp, bytes, cub::CountingInputIterator<uint32_t>(0),
+                                      ptr<uint8_t>(p->touched), list, n_list, (int)NV, s);
+  }));
+  cub::TransformInputIterator<uint32_t, ByteToU32, const uint8_t *> t_it(ptr<uint8_t>(p->touched),
+                                                                        ByteToU32{});
+  TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+    return cub::DeviceScan::ExclusiveSum(tmp, bytes, t_it, ptr<uint32_t>(p->k3_rank), (int)NV, s);
+  }));
+  p->cache_valid = true;
   return TS_OK;
 }
 

@@ -5,7 +5,17 @@
 
 namespace ts {
 
-enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2 };
+enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2, K2_CACHE = 3 };
+
+// Contribution cache of one (gv, 8x8 quadrant) slot (K2_CACHE mode), stored at the start of the
+// slot's Partial record: the kept-contribution pixels of the quadrant as a 64-bit mask and their
+// w = alpha T, in pixel order, at pool[offset ..].  Frame independent: every target frame of a
+// clip reuses it (the reference's weight-map reuse, pipeline.py:191-196).
+struct CacheRec {
+  uint64_t mask;
+  uint32_t offset, count;
+};
+constexpr uint32_t K2_CACHE_CHUNK = 8192;  // pool doubles a warp reserves at a time
 
 constexpr int K1_RECT_OFFSET = 128;  // u32 offset of the per-view bbox unions in the drange buffer
 void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V, int dbits,
@@ -33,7 +43,8 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
                       unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm = 0,
-                      uint8_t *touched = nullptr);
+                      uint8_t *touched = nullptr, double *pool = nullptr,
+                      unsigned long long *pool_cursor = nullptr, uint64_t pool_cap = 0);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
 bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched bytes
 
@@ -44,6 +55,13 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
                      const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
                      void *fits, cudaStream_t s);
 size_t k3_fit_bytes();  // per touched gv, the compact fit record of K3
+// K2+K3 of one target frame from the clip's contribution cache (K2_CACHE records and pool)
+void launch_k23_cached(const void *recs, const double *pool, const uint8_t *flag,
+                       const uint32_t *inst_base, const int16_t *bbox, const uint32_t *list,
+                       const uint32_t *n_list, int64_t n, int64_t nv_total, int W, int H,
+                       const void *tgt, int track_dtype, const uint8_t *val,
+                       const ts_config &cfg, ts_motions m, const uint8_t *touched,
+                       const uint32_t *rank, void *fits, cudaStream_t s);
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
                       int64_t n, double det_floor, int min_pixels, double min_weight,

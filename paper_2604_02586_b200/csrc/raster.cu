@@ -56,6 +56,10 @@ struct K2Params {
   Partial *partial;  // one slot per (gv, 8x8 quadrant of its bbox)
   uint8_t *flag;
   uint8_t *touched;  // per gv: 1 once it has a tracked contribution (zeroed before K2)
+  // cache mode: pool of w values, its cursor (doubles handed out) and capacity
+  double *pool;
+  unsigned long long *pool_cursor;
+  uint64_t pool_cap;
   // emit mode
   unsigned long long *emit_count;
   int64_t emit_cap;
@@ -201,6 +205,57 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
   }
 }
 
+// Cache mode (K2_CACHE): the pending Gaussians' kept contributions -- every pixel that passed the
+// keep predicate with T >= early stop, whatever the tracks -- as (mask, offset) slot records and
+// their w values in pixel order in the pool.  The warp reserves pool space in chunks of
+// K2_CACHE_CHUNK doubles (one atomic per chunk); each flush takes one consecutive range for its
+// Gaussians.  A full pool is reported by the cursor passing the capacity (nothing is written
+// beyond it; the build reruns with a larger pool).  Warp-uniform call.
+template <typename TrackT>
+__device__ __forceinline__ void k2_flush_cache(const K2Warp<TrackT> &S, const K2Params &P,
+                                               int lane, int kcount, uint64_t my_cm,
+                                               uint32_t my_slot, unsigned long long &cur,
+                                               unsigned long long &lim) {
+  const int kk = lane & (K2_FLUSH - 1), qq = lane / K2_FLUSH;
+  const uint32_t cnt = kk < kcount ? (uint32_t)__popcll(my_cm) : 0u;
+  // exclusive prefix of the counts over the K2_FLUSH Gaussians (lanes 0..K2_FLUSH-1 hold them)
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < K2_FLUSH; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (kk >= d) incl += o;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, K2_FLUSH - 1);
+  const uint32_t pre = incl - cnt;
+  if (cur + total > lim) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(P.pool_cursor, (unsigned long long)K2_CACHE_CHUNK);
+    cur = __shfl_sync(0xffffffffu, base, 0);
+    lim = cur + K2_CACHE_CHUNK;
+  }
+  const unsigned long long off = cur + pre;
+  cur += total;
+  if (cnt && off + cnt <= P.pool_cap) {
+    uint64_t bits = my_cm;
+    for (int k = 0; k < qq; k++) bits &= bits - 1;
+    uint32_t r = qq;
+    while (bits) {
+      const int p = __ffsll((long long)bits) - 1;
+#pragma unroll
+      for (int k = 0; k < 4; k++) bits &= bits - 1;
+      P.pool[off + r] = S.w[kk][p];
+      r += 4;
+    }
+    if (qq == 0) {
+      CacheRec *rec = reinterpret_cast<CacheRec *>(P.partial + my_slot);
+      rec->mask = my_cm;
+      rec->offset = (uint32_t)off;
+      rec->count = cnt;
+      P.flag[my_slot] = 1;
+    }
+  }
+}
+
 template <int MODE, typename TrackT>
 __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(const K2Params P) {
   extern __shared__ __align__(16) unsigned char k2_smem_raw[];
@@ -212,6 +267,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
       reinterpret_cast<K2Warp<TrackT> *>(k2_smem_raw + K2_ETAB_BYTES)[warp];
   const uint32_t n_units = 4u * *P.n_items;
   unsigned long long st[K2S_N] = {};
+  constexpr bool kSlots = MODE == K2_ACCUMULATE || MODE == K2_CACHE;
+  unsigned long long pool_cur = 0, pool_lim = 0;  // cache mode: the warp's pool chunk
 
   for (;;) {
     uint32_t unit = 0;
@@ -292,7 +349,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         const uint32_t gv = P.inst_gv[i];
         // the partial-slot base is loaded beside the record (not after the hit test), so the
         // chunk's dependent chain is inst_gv -> {record, slot base}
-        const uint32_t ibase = MODE == K2_ACCUMULATE ? __ldg(P.inst_base + gv) : 0u;
+        const uint32_t ibase = kSlots ? __ldg(P.inst_base + gv) : 0u;
         const RasterRec r = P.rec[gv];
         const uint64_t rect = quad_rect(r, qx0, qy0);
         hit = (rect & ~done64) != 0ull;
@@ -300,7 +357,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
           S.rec[lane] = r;
           S.rect[lane] = rect;
           S.gvid[lane] = gv;
-          if (MODE == K2_ACCUMULATE) {
+          if (kSlots) {
             // one slot per 8x8 quadrant of the gv's bbox, row-major from its top-left quadrant
             const int bx0 = r.x0 >> 3, bx1 = r.x1 >> 3, by0 = r.y0 >> 3;
             S.slot[lane] = ibase + (uint32_t)(((qy0 >> 3) - by0) * (bx1 - bx0 + 1) +
@@ -336,8 +393,11 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
                                      P.early_stop, etab, s1, a1, w1, t1);
           done64 = (uint64_t)__ballot_sync(0xffffffffu, !(s0.T >= P.early_stop)) |
                    ((uint64_t)__ballot_sync(0xffffffffu, !(s1.T >= P.early_stop)) << 32);
-          if (MODE == K2_ACCUMULATE) {
-            const bool k0 = c0 && valid0, k1 = c1 && valid1;
+          if (kSlots) {
+            // accumulate: tracked contributions; cache: every kept contribution (the tracks of
+            // the clip's target frames are applied per frame from the cache)
+            const bool k0 = c0 && (MODE == K2_CACHE || valid0);
+            const bool k1 = c1 && (MODE == K2_CACHE || valid1);
             const uint32_t cm0 = __ballot_sync(0xffffffffu, k0);
             const uint32_t cm1 = __ballot_sync(0xffffffffu, k1);
             if (K2_STATS_ON) {
@@ -359,7 +419,10 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
               if (++kpend == K2_FLUSH) {
                 __syncwarp();
                 if (K2_STATS_ON) st[K2S_FLUSHES]++;
-                k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
+                if (MODE == K2_CACHE)
+                  k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, pool_cur, pool_lim);
+                else
+                  k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
                 __syncwarp();
                 kpend = 0;
                 my_cm = 0;
@@ -401,10 +464,13 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
         }
       }
     }
-    if (MODE == K2_ACCUMULATE && kpend > 0) {
+    if (kSlots && kpend > 0) {
       __syncwarp();
       if (K2_STATS_ON) st[K2S_FLUSHES]++;
-      k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
+      if (MODE == K2_CACHE)
+        k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, pool_cur, pool_lim);
+      else
+        k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
       __syncwarp();
     }
     if (MODE == K2_DOMINANT) {
@@ -500,7 +566,8 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       uint32_t *emit_gv, double *emit_alpha, double *emit_trans,
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
                       unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm,
-                      uint8_t *touched) {
+                      uint8_t *touched, double *pool, unsigned long long *pool_cursor,
+                      uint64_t pool_cap) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -541,6 +608,9 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.partial = partial;
   P.flag = flag;
   P.touched = touched;
+  P.pool = pool;
+  P.pool_cursor = pool_cursor;
+  P.pool_cap = pool_cap;
   P.emit_count = emit_count;
   P.emit_cap = emit_cap;
   P.emit_key = emit_key;
@@ -555,6 +625,7 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
     if (track_dtype == TS_TRACK_F32) return launch_mode<K2_ACCUMULATE, float>(P, s, ctas_per_sm);
     return launch_mode<K2_ACCUMULATE, double>(P, s, ctas_per_sm);
   }
+  if (mode == K2_CACHE) return launch_mode<K2_CACHE, float>(P, s, ctas_per_sm);
   if (mode == K2_EMIT) return launch_mode<K2_EMIT, float>(P, s, ctas_per_sm);
   return launch_mode<K2_DOMINANT, float>(P, s, ctas_per_sm);
 }

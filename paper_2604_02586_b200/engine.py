@@ -182,6 +182,23 @@ class FrameEngine:
                     status=grab(b.gv_status, nv, np.int8),
                     bbox=grab(b.gv_bbox, nv, np.int16, 4))
 
+    def build_cache(self, stream=None):
+        """Rasterize the current binning once WITHOUT tracks and keep every contribution (pixel,
+        w = alpha T) for the clip: later compensate() calls apply each target frame's tracks to
+        the cache instead of re-rasterizing (the reference reuses the frame-0 weight maps across
+        a clip's target frames, pipeline.py:191-196).  Valid until the next bin()."""
+        plans = [self.plan] if not self.grouped else [g[2] for g in self._groups]
+        for plan in plans:
+            nat.check(self._lib.ts_frame_cache(plan.handle, 1, nat.stream_ptr(stream)),
+                      "ts_frame_cache")
+        return self
+
+    def drop_cache(self):
+        plans = [self.plan] if not self.grouped else [g[2] for g in self._groups]
+        for plan in plans:
+            nat.check(self._lib.ts_frame_cache(plan.handle, 0, None), "ts_frame_cache")
+        return self
+
     def track_rects(self):
         """(V, 4) int32 inclusive pixel rectangles (x0, y0, x1, y1) the next compensate reads."""
         if self.grouped:
