@@ -271,9 +271,10 @@ def run_pipeline(scene, clip_len, workers=1, config: Config = None, mode="short"
 
     Per clip: the tracker's binning of the ground-truth first frame (K1) is reused for the
     compensation when the clip starts from ground truth (short mode, or the first clip of a
-    chain) -- the reference's weight-map reuse (:191-196); the exact kNN is built once per clip on
-    the device; every target frame then runs the GPU oracle tracker, K2-K4 and the regularisation
-    kernels.  Long mode chains clips through the previous clip's estimate of its last frame.
+    chain) -- the reference's weight-map reuse (:191-196), which also covers the rasterization:
+    with several target frames the contributions are cached once per clip (ts_frame_cache); the
+    exact kNN is built once per clip on the device; every target frame then runs the GPU oracle
+    tracker, K2+K3 from the cache (or K2-K3), K4 and the regularisation kernels.  Long mode chains clips through the previous clip's estimate of its last frame.
 
     `workers` is accepted for signature parity (>= 1); parallelism comes from the GPU and, when
     torch.distributed is initialised with more than one rank (`group`), from frame sharding:
@@ -322,9 +323,14 @@ def run_pipeline(scene, clip_len, workers=1, config: Config = None, mode="short"
             eng = eng_comp.bin(first_rows, cams, config)
         g_dev = eng._gauss
         adj = knn_device(g_dev, config.knn_k)
+        mine = frames_for_rank(clip.target_frames, rank, world)
+        if len(mine) > 1:
+            # the clip's target frames share frame 0's contributions: rasterize once
+            # (the reference's weight-map reuse, :191-196) and apply each frame's tracks
+            eng.build_cache()
         torch.cuda.synchronize()
         stage_totals["setup"] += time.perf_counter() - t0
-        for f in frames_for_rank(clip.target_frames, rank, world):
+        for f in mine:
             t0 = time.perf_counter()
             tgt, val = oracle_tracks(scene, f, noise_sigma_px, seed, first_frame=clip.first_frame,
                                      engine=eng_track)
