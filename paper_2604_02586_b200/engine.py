@@ -572,8 +572,11 @@ class StreamingEngine:
             # binning instead (off the frame's critical path; cfg3: 56 MB vs 29 MB of rectangles)
             whole = t_host.numel() * t_host.element_size() + v_host.numel()
             rect = whole > 2 * self._rect_bytes
-        zero_copy = not rect and self._choose_zero_copy(g_host, t_host, v_host) and \
-            _pinned_pair(t_host, v_host)
+        if self.zero_copy_tracks == "rect":
+            zero_copy = False  # rectangles after the binning, or the whole arrays now
+        else:
+            zero_copy = self._choose_zero_copy(g_host, t_host, v_host) and \
+                _pinned_pair(t_host, v_host)
         if rect:
             self.steps_rect_copy += 1
         elif zero_copy:

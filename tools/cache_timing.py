@@ -1,0 +1,63 @@
+"""Per-stage timing of a clip with and without the contribution cache.
+
+    python tools/cache_timing.py --config cfg5 --frames 8
+
+Prints the cache build time and, per target frame, the CUDA-event stage times (the cached path
+reports K2+K3 under k3_solve and 0 under k2_raster_accumulate).  NVTX ranges "build" / "frame"
+for ncu captures.
+"""
+
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    import bench
+    from paper_2604_02586_b200.engine import FrameEngine
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--frames", type=int, default=8)
+    args = ap.parse_args()
+    c = bench.CONFIGS[args.config]
+    frames = [c["gap"] * (j + 1) for j in range(args.frames)]
+    scene, tracks = bench.make_inputs(args.config, frames[-1] + 1, frames=frames)
+    g = torch.as_tensor(scene.frames[0], device="cuda")
+    eng = FrameEngine()
+    eng.bin(g, scene.cameras)
+    outs = {f: eng.compensate(*tracks[f]) for f in frames}  # warm-up, allocations
+    for use_cache in (False, True):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        torch.cuda.nvtx.range_push("build")
+        eng.bin(g, scene.cameras)
+        if use_cache:
+            eng.build_cache()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+        t_build = time.perf_counter() - t0
+        eng.plan.timing(True)
+        t0 = time.perf_counter()
+        for f in frames:
+            torch.cuda.nvtx.range_push("frame")
+            outs[f] = eng.compensate(*tracks[f], outs[f])
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        t_frames = time.perf_counter() - t0
+        st = eng.plan.timing_read()
+        eng.plan.timing(False)
+        print(f"cache={use_cache}: bin{'+cache' if use_cache else ''} {1e3 * t_build:.2f} ms, "
+              f"{len(frames)} frames {1e3 * t_frames:.2f} ms wall; stage ms/frame:",
+              {k: round(v[0] / max(v[1], 1), 3) for k, v in st.items()}, flush=True)
+        if use_cache:
+            eng.drop_cache()
+
+
+if __name__ == "__main__":
+    main()
