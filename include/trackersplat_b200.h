@@ -152,13 +152,15 @@ int ts_frame_binning(const ts_plan *plan, ts_binning *out);
 int ts_frame_occupied_tiles(const ts_plan *plan, int64_t *out);
 
 /* Clip contribution cache (enable = 1): runs K2 once over the current binning WITHOUT tracks and
- * keeps every kept contribution (pixel, w = alpha T) per (Gaussian-view, 8x8 quadrant) in the
- * plan; until the next ts_frame_bin (or enable = 0), ts_frame_compensate then skips the
- * rasterization and applies each target frame's tracks to the cached contributions (K2 + K3 in
- * one pass) -- the GPU form of the reference's frame-0 weight-map reuse across a clip's target
- * frames (pipeline.py:191-196; compensate_frame(weightmaps=...), pipeline.py:110-116).
+ * keeps every kept contribution (pixel, w = alpha T) as one record per (Gaussian-view, 8x8
+ * quadrant) in the plan; until the next ts_frame_bin (or enable = 0), ts_frame_compensate then
+ * skips the rasterization and turns each record into its moments with the target frame's tracks
+ * -- the GPU form of the reference's frame-0 weight-map reuse across a clip's target frames
+ * (pipeline.py:191-196; compensate_frame(weightmaps=...), pipeline.py:110-116).
  * Synchronous (sizes the pool); TS_E_CAPACITY if the pool cannot be sized. */
 int ts_frame_cache(ts_plan *plan, int32_t enable, void *stream);
+/* Size of the current cache: records (32 B each) and cached w values (8 B each); 0 when none. */
+int ts_frame_cache_info(const ts_plan *plan, uint64_t *n_records, uint64_t *n_values);
 
 /* Per view, the pixel rectangle the next ts_frame_compensate reads from the track arrays (the
  * 16x16 tiles touched by any binned bbox; inclusive x0 y0 x1 y1, x1 < x0 when the view has no

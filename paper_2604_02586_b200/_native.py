@@ -102,6 +102,8 @@ _SIGS = {
     "ts_frame_occupied_tiles": ([_vp, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "ts_frame_track_rects": ([_vp, _vp], ctypes.c_int),
     "ts_frame_cache": ([_vp, ctypes.c_int32, _vp], ctypes.c_int),
+    "ts_frame_cache_info": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
+                            ctypes.c_int),
     "ts_copy_track_rects": ([_vp, _vp, ctypes.c_int32, _vp, _vp, _vp, _vp], ctypes.c_int),
     "ts_rasterize_weights": ([_vp, _vp, ctypes.c_int64, ctypes.POINTER(Camera), ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_int64),

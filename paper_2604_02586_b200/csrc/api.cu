@@ -72,7 +72,7 @@ struct ts_plan {
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf k2_stats;
-  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, cache_pool, cache_cursor, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
+  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, cache_pool, cache_cursor, cache_recs, cache_cnt, cache_off, cache_w, cache_xy, cache_ranges, cache_chunks, cache_multi, cache_scratch, cache_counters, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
       mot_sw;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
@@ -93,6 +93,9 @@ struct ts_plan {
   bool cache_valid = false;  // clip contribution cache (ts_frame_cache) of the current binning
   uint64_t cache_cap = 0;    // pool capacity in doubles
   uint64_t cache_used = 0;   // doubles handed out by the last build
+  uint64_t cache_rec_cap = 0;  // record capacity
+  uint64_t cache_recs_used = 0;  // records handed out by the last build (incl. unfilled)
+  uint64_t cache_chunk_bound = 0, cache_multi_bound = 0;  // work units of the per-frame kernel
   bool k3_last_split = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_marks;
@@ -142,7 +145,7 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
                           &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                           &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                          &p->tie_tmp, &p->cache_pool, &p->cache_cursor};
+                          &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs, &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy, &p->cache_ranges, &p->cache_chunks, &p->cache_multi, &p->cache_scratch, &p->cache_counters};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -161,7 +164,7 @@ void release_all(ts_plan *p) {
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
                     &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                     &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                    &p->tie_tmp, &p->cache_pool, &p->cache_cursor};
+                    &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs, &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy, &p->cache_ranges, &p->cache_chunks, &p->cache_multi, &p->cache_scratch, &p->cache_counters};
   for (DevBuf *b : bufs) b->release();
 }
 
@@ -621,17 +624,21 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.weight_sum) m.weight_sum = im.weight_sum;
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
-  if (p->cache_valid) {
-    // the clip's contribution cache: K2 + K3 as one pass over the cached contributions with
-    // this frame's tracks (no rasterization), then K4
+  const bool cached = p->cache_valid;
+  if (cached) {
+    // the clip's contribution cache: this frame's moments and fits straight from the cached
+    // contributions (no rasterization, no partials); list, ranks and ranges set by ts_frame_cache
+    uint32_t *list = ptr<uint32_t>(p->k3_list);
     cudaEvent_t e3 = p->mark_begin(s);
+    TS_CUDA_TRY(launch_k23_cached(p->cache_chunks.p, ptr<uint32_t>(p->cache_counters),
+                                  p->cache_chunk_bound, p->cache_multi.p, p->cache_multi_bound,
+                                  list, ptr<int16_t>(p->bbox), n, p->W, p->H,
+                                  ptr<double>(p->cache_w), ptr<uint32_t>(p->cache_xy),
+                                  track_target, track_dtype, track_valid, p->cfg, p->k3_fits.p,
+                                  ptr<double>(p->cache_scratch), s));
     p->mark_end(ST_RASTER, e3, s);
     cudaEvent_t e4 = p->mark_begin(s);
-    uint32_t *list = ptr<uint32_t>(p->k3_list);
-    launch_k23_cached(p->partial.p, ptr<double>(p->cache_pool), ptr<uint8_t>(p->flag),
-                      ptr<uint32_t>(p->inst_base), ptr<int16_t>(p->bbox), list, list + NV + 4, n,
-                      NV, p->W, p->H, track_target, track_dtype, track_valid, p->cfg, m,
-                      ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, s);
+    launch_k3_merge(ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, NV, m, s);
     TS_CUDA_TRY(cudaGetLastError());
     p->mark_end(ST_SOLVE, e4, s);
   } else {
@@ -731,18 +738,24 @@ int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
   ENSURE(p->k3_rank, 4 * (NV + 8));
   ENSURE(p->k3_fits, k3_fit_bytes() * (NV + 1));
   ENSURE(p->k2_sched, k2_schedule_bytes(p->tpv * p->V));
-  ENSURE(p->cache_cursor, 8);
+  ENSURE(p->cache_cursor, 16);  // [0] pool doubles handed out, [1] records handed out
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // every K2 warp may leave most of one chunk unused
-  const uint64_t slack = (uint64_t)sms * 8 * 4 * K2_CACHE_CHUNK;
-  if (p->cache_cap == 0) p->cache_cap = (uint64_t)std::max<int64_t>(8 * ns, 1 << 22) + slack;
+  // every K2 warp may leave most of one pool chunk and one record chunk unused
+  const uint64_t warps = (uint64_t)sms * 8 * 4;
+  const uint64_t slack = warps * K2_CACHE_CHUNK, rslack = warps * K2_CACHE_RECS;
+  if (p->cache_cap == 0) p->cache_cap = (uint64_t)std::max<int64_t>(4 * ns, 1 << 22) + slack;
+  if (p->cache_rec_cap == 0) p->cache_rec_cap = (uint64_t)std::max<int64_t>(ns / 2, 1 << 16) + rslack;
+  unsigned long long *cur = ptr<unsigned long long>(p->cache_cursor);
   for (int attempt = 0; attempt < 3; attempt++) {
     ENSURE(p->cache_pool, 8 * p->cache_cap);
+    ENSURE(p->cache_recs, sizeof(CacheRec) * p->cache_rec_cap);
     TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
     TS_CUDA_TRY(cudaMemsetAsync(p->touched.p, 0, NV + 8, s));
-    TS_CUDA_TRY(cudaMemsetAsync(p->cache_cursor.p, 0, 8, s));
+    TS_CUDA_TRY(cudaMemsetAsync(cur, 0, 16, s));
+    // reserved records no warp fills stay mask 0 (skipped per frame)
+    TS_CUDA_TRY(cudaMemsetAsync(p->cache_recs.p, 0, sizeof(CacheRec) * p->cache_rec_cap, s));
     TS_CUDA_TRY(launch_k2(K2_CACHE, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
                           ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
                           ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0,
@@ -750,16 +763,20 @@ int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
                           p->cfg, ptr<Partial>(p->partial), ptr<uint8_t>(p->flag), nullptr, 0,
                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                           p->k2_sched.p, s, p->k2_ctas_per_sm, ptr<uint8_t>(p->touched),
-                          ptr<double>(p->cache_pool),
-                          ptr<unsigned long long>(p->cache_cursor), p->cache_cap));
-    uint64_t used = 0;
-    TS_CUDA_TRY(cudaMemcpyAsync(&used, p->cache_cursor.p, 8, cudaMemcpyDeviceToHost, s));
+                          ptr<double>(p->cache_pool), cur, p->cache_cap,
+                          ptr<CacheRec>(p->cache_recs), cur + 1, p->cache_rec_cap));
+    uint64_t used[2] = {0, 0};
+    TS_CUDA_TRY(cudaMemcpyAsync(used, cur, 16, cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
-    if (used <= p->cache_cap) {
-      p->cache_used = used;
+    const bool pool_ok = used[0] <= p->cache_cap, recs_ok = used[1] <= p->cache_rec_cap;
+    if (pool_ok && recs_ok) {
+      p->cache_used = used[0];
+      p->cache_recs_used = used[1];
       break;
     }
-    p->cache_cap = used + used / 8 + slack;  // pool too small: grow and rebuild
+    // too small: grow and rebuild
+    if (!pool_ok) p->cache_cap = used[0] + used[0] / 8 + slack;
+    if (!recs_ok) p->cache_rec_cap = used[1] + used[1] / 8 + rslack;
     if (attempt == 2) return TS_E_CAPACITY;
   }
   // the touched gvs (any cached contribution) and their ranks: fixed for the clip
@@ -773,7 +790,59 @@ int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
   TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
     return cub::DeviceScan::ExclusiveSum(tmp, bytes, t_it, ptr<uint32_t>(p->k3_rank), (int)NV, s);
   }));
+  // the records in slot order: per-slot counts, their offsets, the contributions scattered
+  // there (every gv's run contiguous), the run of every listed gv
+  if (p->cache_used >= (uint64_t)1 << 32) return TS_E_CAPACITY;  // 32-bit contribution offsets
+  ENSURE(p->cache_cnt, 4 * (ns + 1));
+  ENSURE(p->cache_off, 4 * (ns + 1));
+  ENSURE(p->cache_w, 8 * (p->cache_used + 1));
+  ENSURE(p->cache_xy, 4 * (p->cache_used + 1));
+  ENSURE(p->cache_ranges, 8 * (NV + 1));
+  TS_CUDA_TRY(cudaMemsetAsync(p->cache_cnt.p, 0, 4 * (ns + 1), s));
+  launch_cache_slot_counts(ptr<CacheRec>(p->cache_recs), cur + 1, p->cache_rec_cap,
+                           ptr<uint32_t>(p->cache_cnt), s);
+  TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+    return cub::DeviceScan::ExclusiveSum(tmp, bytes, ptr<uint32_t>(p->cache_cnt),
+                                         ptr<uint32_t>(p->cache_off), (int)(ns + 1), s);
+  }));
+  launch_cache_scatter(ptr<CacheRec>(p->cache_recs), cur + 1, p->cache_rec_cap,
+                       ptr<double>(p->cache_pool), ptr<uint32_t>(p->cache_off),
+                       ptr<double>(p->cache_w), ptr<uint32_t>(p->cache_xy), s);
+  launch_cache_ranges(list, n_list, NV, ptr<int16_t>(p->bbox), ptr<uint32_t>(p->inst_base),
+                      ptr<uint32_t>(p->cache_off), ptr<uint2>(p->cache_ranges), s);
+  // the per-frame work units: every gv's run cut into chunks of at most cache_chunk_len()
+  uint32_t counts[2] = {0, 0};  // touched gvs, cached contributions
+  TS_CUDA_TRY(cudaMemcpyAsync(counts, n_list, 4, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(cudaMemcpyAsync(counts + 1, ptr<uint32_t>(p->cache_off) + ns, 4,
+                              cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(cudaStreamSynchronize(s));
+  const uint64_t nl = counts[0], total = counts[1], cl = (uint64_t)cache_chunk_len();
+  p->cache_chunk_bound = nl + total / cl + 1;
+  p->cache_multi_bound = total / cl + 1;  // a split gv holds more than cl contributions
+  uint32_t *nch = ptr<uint32_t>(p->cache_cnt), *choff = ptr<uint32_t>(p->cache_off);  // reused
+  ENSURE(p->cache_chunks, cache_chunk_bytes() * p->cache_chunk_bound);
+  ENSURE(p->cache_multi, cache_multi_bytes() * p->cache_multi_bound);
+  ENSURE(p->cache_scratch, cache_scratch_bytes() * (2 * total / cl + 1));
+  ENSURE(p->cache_counters, 16);
+  TS_CUDA_TRY(cudaMemsetAsync(nch, 0, 4 * (nl + 1), s));
+  TS_CUDA_TRY(cudaMemsetAsync(p->cache_counters.p, 0, 16, s));
+  launch_cache_chunk_counts(n_list, NV, ptr<uint2>(p->cache_ranges), nch, s);
+  TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
+    return cub::DeviceScan::ExclusiveSum(tmp, bytes, nch, choff, (int)(nl + 1), s);
+  }));
+  launch_cache_chunk_fill(list, n_list, NV, ptr<int16_t>(p->bbox), n,
+                          ptr<uint2>(p->cache_ranges), nch, choff,
+                          p->cache_chunks.p, p->cache_multi.p,
+                          ptr<uint32_t>(p->cache_counters), s);
+  TS_CUDA_TRY(cudaGetLastError());
   p->cache_valid = true;
+  return TS_OK;
+}
+
+int ts_frame_cache_info(const ts_plan *p, uint64_t *n_records, uint64_t *n_values) {
+  if (!p || !n_records || !n_values) return TS_E_INVALID_ARGUMENT;
+  *n_records = p->cache_valid ? p->cache_recs_used : 0;
+  *n_values = p->cache_valid ? p->cache_used : 0;
   return TS_OK;
 }
 

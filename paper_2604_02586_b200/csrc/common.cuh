@@ -257,6 +257,23 @@ TS_HD bool is_static(double u, double v, int px, int py, double thr) {
   return sqrt_rn(add(mul(d0, d0), mul(d1, d1))) < thr;
 }
 
+// The same test without the square root: a correctly rounded sqrt is monotone, so
+// {x : sqrt_rn(x) < thr} = [0, L] (or empty) and sqrt_rn(x) < thr <=> x <= L exactly; L is found
+// on the host with its (IEEE, correctly rounded) sqrt.  NaN compares false on both sides.
+inline double static_sq_limit(double thr) {
+  if (!(thr > 0.0)) return -1.0;  // never static (x >= 0)
+  if (std::isinf(thr)) return 1.7976931348623157e308;  // every finite x
+  double x = thr * thr;
+  if (std::isinf(x)) x = 1.7976931348623157e308;
+  while (x > 0.0 && !(std::sqrt(x) < thr)) x = std::nextafter(x, 0.0);
+  while (std::sqrt(std::nextafter(x, HUGE_VAL)) < thr) x = std::nextafter(x, HUGE_VAL);
+  return x;
+}
+TS_HD bool is_static_sq(double u, double v, int px, int py, double lim) {
+  double d0 = sub(u, (double)px), d1 = sub(v, (double)py);
+  return add(mul(d0, d0), mul(d1, d1)) <= lim;
+}
+
 // Moments of one Gaussian in one tile, relative to the integer anchor
 // ((x0+x1)>>1, (y0+y1)>>1) of its view bbox:  h = [dx, dy, 1], x'_a = x' - anchor.
 //  0 S, 1 Sx, 2 Sy, 3 Sxx, 4 Sxy, 5 Syy, 6 Su, 7 Sv, 8 Sxu, 9 Sxv, 10 Syu, 11 Syv, 12 Sstatic_w

@@ -7,14 +7,19 @@ namespace ts {
 
 enum { K2_ACCUMULATE = 0, K2_EMIT = 1, K2_DOMINANT = 2, K2_CACHE = 3 };
 
-// Contribution cache of one (gv, 8x8 quadrant) slot (K2_CACHE mode), stored at the start of the
-// slot's Partial record: the kept-contribution pixels of the quadrant as a 64-bit mask and their
-// w = alpha T, in pixel order, at pool[offset ..].  Frame independent: every target frame of a
-// clip reuses it (the reference's weight-map reuse, pipeline.py:191-196).
+// Contribution cache record of one (gv, 8x8 quadrant) slot with kept contributions (K2_CACHE
+// mode): the quadrant's kept-contribution pixels as a 64-bit mask, their w = alpha T in pixel
+// order at pool[offset ..], the slot, the quadrant origin, the moment anchor and the view.  Frame
+// independent: every target frame of a clip reuses it (the reference's weight-map reuse,
+// pipeline.py:191-196); per frame k2_cached turns each record into the slot's Partial.
 struct CacheRec {
   uint64_t mask;
-  uint32_t offset, count;
+  uint32_t offset, slot;
+  int16_t qx0, qy0, ax, ay;
+  int32_t view, pad;
 };
+static_assert(sizeof(CacheRec) == 32, "CacheRec is 32 bytes");
+constexpr uint32_t K2_CACHE_RECS = 256;  // records a warp reserves at a time
 constexpr uint32_t K2_CACHE_CHUNK = 8192;  // pool doubles a warp reserves at a time
 
 constexpr int K1_RECT_OFFSET = 128;  // u32 offset of the per-view bbox unions in the drange buffer
@@ -44,7 +49,38 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
                       unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm = 0,
                       uint8_t *touched = nullptr, double *pool = nullptr,
-                      unsigned long long *pool_cursor = nullptr, uint64_t pool_cap = 0);
+                      unsigned long long *pool_cursor = nullptr, uint64_t pool_cap = 0,
+                      CacheRec *recs = nullptr, unsigned long long *rec_cursor = nullptr,
+                      uint64_t rec_cap = 0);
+// per target frame: every cache record -> its slot's Partial with this frame's tracks
+// Clip cache (cache.cu): records -> contributions in slot order (cw, cxy) and per-gv ranges over
+// the touched list, once per clip; per target frame the moments + fits of the listed gvs.
+void launch_cache_slot_counts(const CacheRec *recs, const unsigned long long *n_recs,
+                              uint64_t rec_cap, uint32_t *slot_cnt, cudaStream_t s);
+void launch_cache_scatter(const CacheRec *recs, const unsigned long long *n_recs, uint64_t rec_cap,
+                          const double *pool, const uint32_t *slot_off, double *cw, uint32_t *cxy,
+                          cudaStream_t s);
+void launch_cache_ranges(const uint32_t *list, const uint32_t *n_list, int64_t nv_total,
+                         const int16_t *bbox, const uint32_t *inst_base, const uint32_t *slot_off,
+                         uint2 *ranges, cudaStream_t s);
+size_t cache_chunk_bytes();
+size_t cache_multi_bytes();
+size_t cache_scratch_bytes();
+int cache_chunk_len();
+void launch_cache_chunk_counts(const uint32_t *n_list, int64_t nv_total, const uint2 *ranges,
+                               uint32_t *nch, cudaStream_t s);
+void launch_cache_chunk_fill(const uint32_t *list, const uint32_t *n_list, int64_t nv_total,
+                             const int16_t *bbox, int64_t n, const uint2 *ranges,
+                             const uint32_t *nch, const uint32_t *choff, void *chunks, void *multi,
+                             uint32_t *counters, cudaStream_t s);
+cudaError_t launch_k23_cached(const void *chunks, const uint32_t *counters, uint64_t chunk_bound,
+                              const void *multi, uint64_t multi_bound, const uint32_t *list,
+                              const int16_t *bbox, int64_t n, int W, int H, const double *cw,
+                              const uint32_t *cxy, const void *track_target, int track_dtype,
+                              const uint8_t *track_valid, const ts_config &cfg, void *fits,
+                              double *scratch, cudaStream_t s);
+void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
+                     int64_t nv_total, ts_motions m, cudaStream_t s);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
 bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched bytes
 
@@ -55,13 +91,7 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
                      const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
                      void *fits, cudaStream_t s);
 size_t k3_fit_bytes();  // per touched gv, the compact fit record of K3
-// K2+K3 of one target frame from the clip's contribution cache (K2_CACHE records and pool)
-void launch_k23_cached(const void *recs, const double *pool, const uint8_t *flag,
-                       const uint32_t *inst_base, const int16_t *bbox, const uint32_t *list,
-                       const uint32_t *n_list, int64_t n, int64_t nv_total, int W, int H,
-                       const void *tgt, int track_dtype, const uint8_t *val,
-                       const ts_config &cfg, ts_motions m, const uint8_t *touched,
-                       const uint32_t *rank, void *fits, cudaStream_t s);
+
 // solve_view on absolute moments (stage API)
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
                       int64_t n, double det_floor, int min_pixels, double min_weight,

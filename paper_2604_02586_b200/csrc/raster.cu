@@ -56,10 +56,13 @@ struct K2Params {
   Partial *partial;  // one slot per (gv, 8x8 quadrant of its bbox)
   uint8_t *flag;
   uint8_t *touched;  // per gv: 1 once it has a tracked contribution (zeroed before K2)
-  // cache mode: pool of w values, its cursor (doubles handed out) and capacity
+  // cache mode: pool of w values, its cursor (doubles handed out) and capacity; the records
   double *pool;
   unsigned long long *pool_cursor;
   uint64_t pool_cap;
+  CacheRec *recs;
+  unsigned long long *rec_cursor;
+  uint64_t rec_cap;
   // emit mode
   unsigned long long *emit_count;
   int64_t emit_cap;
@@ -206,36 +209,53 @@ __device__ __forceinline__ void k2_flush(const K2Warp<TrackT> &S, const K2Params
 }
 
 // Cache mode (K2_CACHE): the pending Gaussians' kept contributions -- every pixel that passed the
-// keep predicate with T >= early stop, whatever the tracks -- as (mask, offset) slot records and
-// their w values in pixel order in the pool.  The warp reserves pool space in chunks of
-// K2_CACHE_CHUNK doubles (one atomic per chunk); each flush takes one consecutive range for its
-// Gaussians.  A full pool is reported by the cursor passing the capacity (nothing is written
-// beyond it; the build reruns with a larger pool).  Warp-uniform call.
+// keep predicate with T >= early stop, whatever the tracks -- as one CacheRec per (gv, quadrant)
+// and their w values in pixel order in the pool.  The warp reserves pool space in chunks of
+// K2_CACHE_CHUNK doubles and records in chunks of K2_CACHE_RECS (one atomic per chunk); record
+// order does not matter (each one rewrites its own slot per frame).  Running past a capacity is
+// reported by the cursor (nothing is written beyond it; the build reruns larger).  The slot
+// flags (K3's "has a partial") and touched bytes are set here once for the clip.
+struct CacheChunks {
+  unsigned long long pool_cur = 0, pool_lim = 0, rec_cur = 0, rec_lim = 0;
+};
+
 template <typename TrackT>
 __device__ __forceinline__ void k2_flush_cache(const K2Warp<TrackT> &S, const K2Params &P,
                                                int lane, int kcount, uint64_t my_cm,
-                                               uint32_t my_slot, unsigned long long &cur,
-                                               unsigned long long &lim) {
+                                               uint32_t my_slot, int my_ax, int my_ay, int qx0,
+                                               int qy0, int view, CacheChunks &ch) {
   const int kk = lane & (K2_FLUSH - 1), qq = lane / K2_FLUSH;
   const uint32_t cnt = kk < kcount ? (uint32_t)__popcll(my_cm) : 0u;
-  // exclusive prefix of the counts over the K2_FLUSH Gaussians (lanes 0..K2_FLUSH-1 hold them)
-  uint32_t incl = cnt;
+  // exclusive prefix of the counts (and of the record count) over the K2_FLUSH Gaussians
+  uint32_t incl = cnt, rincl = cnt ? 1u : 0u;
 #pragma unroll
   for (int d = 1; d < K2_FLUSH; d <<= 1) {
     const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-    if (kk >= d) incl += o;
+    const uint32_t ro = __shfl_up_sync(0xffffffffu, rincl, d);
+    if (kk >= d) {
+      incl += o;
+      rincl += ro;
+    }
   }
   const uint32_t total = __shfl_sync(0xffffffffu, incl, K2_FLUSH - 1);
-  const uint32_t pre = incl - cnt;
-  if (cur + total > lim) {
+  const uint32_t rtotal = __shfl_sync(0xffffffffu, rincl, K2_FLUSH - 1);
+  if (ch.pool_cur + total > ch.pool_lim) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(P.pool_cursor, (unsigned long long)K2_CACHE_CHUNK);
-    cur = __shfl_sync(0xffffffffu, base, 0);
-    lim = cur + K2_CACHE_CHUNK;
+    ch.pool_cur = __shfl_sync(0xffffffffu, base, 0);
+    ch.pool_lim = ch.pool_cur + K2_CACHE_CHUNK;
   }
-  const unsigned long long off = cur + pre;
-  cur += total;
-  if (cnt && off + cnt <= P.pool_cap) {
+  if (ch.rec_cur + rtotal > ch.rec_lim) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(P.rec_cursor, (unsigned long long)K2_CACHE_RECS);
+    ch.rec_cur = __shfl_sync(0xffffffffu, base, 0);
+    ch.rec_lim = ch.rec_cur + K2_CACHE_RECS;
+  }
+  const unsigned long long off = ch.pool_cur + (incl - cnt);
+  const unsigned long long ri = ch.rec_cur + (rincl - (cnt ? 1u : 0u));
+  ch.pool_cur += total;
+  ch.rec_cur += rtotal;
+  if (cnt && off + cnt <= P.pool_cap && ri < P.rec_cap) {
     uint64_t bits = my_cm;
     for (int k = 0; k < qq; k++) bits &= bits - 1;
     uint32_t r = qq;
@@ -247,10 +267,17 @@ __device__ __forceinline__ void k2_flush_cache(const K2Warp<TrackT> &S, const K2
       r += 4;
     }
     if (qq == 0) {
-      CacheRec *rec = reinterpret_cast<CacheRec *>(P.partial + my_slot);
-      rec->mask = my_cm;
-      rec->offset = (uint32_t)off;
-      rec->count = cnt;
+      CacheRec rec;
+      rec.mask = my_cm;
+      rec.offset = (uint32_t)off;
+      rec.slot = my_slot;
+      rec.qx0 = (int16_t)qx0;
+      rec.qy0 = (int16_t)qy0;
+      rec.ax = (int16_t)my_ax;
+      rec.ay = (int16_t)my_ay;
+      rec.view = view;
+      rec.pad = 0;
+      P.recs[ri] = rec;
       P.flag[my_slot] = 1;
     }
   }
@@ -268,7 +295,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
   const uint32_t n_units = 4u * *P.n_items;
   unsigned long long st[K2S_N] = {};
   constexpr bool kSlots = MODE == K2_ACCUMULATE || MODE == K2_CACHE;
-  unsigned long long pool_cur = 0, pool_lim = 0;  // cache mode: the warp's pool chunk
+  CacheChunks cache_ch;  // cache mode: the warp's pool / record chunks
 
   for (;;) {
     uint32_t unit = 0;
@@ -420,7 +447,8 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
                 __syncwarp();
                 if (K2_STATS_ON) st[K2S_FLUSHES]++;
                 if (MODE == K2_CACHE)
-                  k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, pool_cur, pool_lim);
+                  k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0, v,
+                                 cache_ch);
                 else
                   k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
                 __syncwarp();
@@ -468,7 +496,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
       __syncwarp();
       if (K2_STATS_ON) st[K2S_FLUSHES]++;
       if (MODE == K2_CACHE)
-        k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, pool_cur, pool_lim);
+        k2_flush_cache(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, qx0, qy0, v, cache_ch);
       else
         k2_flush(S, P, lane, kpend, my_cm, my_slot, my_ax, my_ay, static64, qx0, qy0);
       __syncwarp();
@@ -567,7 +595,8 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
                       const double *depth64, int64_t *dom_gid, double *dom_depth,
                       unsigned long long *stats, void *schedule_ws, cudaStream_t s, int ctas_per_sm,
                       uint8_t *touched, double *pool, unsigned long long *pool_cursor,
-                      uint64_t pool_cap) {
+                      uint64_t pool_cap, CacheRec *recs, unsigned long long *rec_cursor,
+                      uint64_t rec_cap) {
   // counters[0] = number of items, counters[1] = work queue head
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -611,6 +640,9 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
   P.pool = pool;
   P.pool_cursor = pool_cursor;
   P.pool_cap = pool_cap;
+  P.recs = recs;
+  P.rec_cursor = rec_cursor;
+  P.rec_cap = rec_cap;
   P.emit_count = emit_count;
   P.emit_cap = emit_cap;
   P.emit_key = emit_key;

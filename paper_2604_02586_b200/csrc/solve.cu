@@ -179,101 +179,6 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
   }
 }
 
-// K2+K3 from the clip's contribution cache (K2_CACHE records, built once per clip): for every
-// listed gv, its cached contributions are walked slot by slot in pixel order, the target frame's
-// tracks applied (motion2d.py:144-160: kept only where the track is valid; static test), and
-// the anchored moments solved (motion2d.py:164-184) -- the rasterization is not repeated per
-// target frame, as the reference reuses the frame-0 weight maps within a clip
-// (pipeline.py:191-196).  Fits go to the compact array in list order (k3_merge then writes the
-// dense motions).
-template <typename TrackT>
-__global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k23_cached(
-    const CacheRec *__restrict__ recs, const double *__restrict__ pool,
-    const uint8_t *__restrict__ flag, const uint32_t *__restrict__ inst_base,
-    const int16_t *__restrict__ bbox, const uint32_t *__restrict__ list,
-    const uint32_t *__restrict__ n_list, int64_t n, int W, int H, const TrackT *__restrict__ tgt,
-    const uint8_t *__restrict__ val, double static_thr, double det_floor, int min_pixels,
-    double min_weight, GvMotion *__restrict__ fits) {
-  const uint32_t nl = *n_list;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
-    const int64_t gv = list[i];
-    const short4 bb = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
-    const int bx0 = bb.x >> 3, by0 = bb.z >> 3;
-    const int nqx = (bb.y >> 3) - bx0 + 1, nqy = (bb.w >> 3) - by0 + 1;
-    const uint32_t sb = inst_base[gv];
-    const int ax = ((int)bb.x + (int)bb.y) >> 1, ay = ((int)bb.z + (int)bb.w) >> 1;
-    const double fax = (double)ax, fay = (double)ay;
-    const int64_t vbase = (gv / n) * (int64_t)H * W;
-    double m[TS_NMOM];
-#pragma unroll
-    for (int k = 0; k < TS_NMOM; k++) m[k] = 0.0;
-    uint32_t cnt = 0, scnt = 0;
-    for (int q = 0; q < nqx * nqy; q++) {
-      if (!flag[sb + q]) continue;
-      const CacheRec rec = recs[(size_t)(sb + q) * (sizeof(Partial) / sizeof(CacheRec))];
-      const int qy = q / nqx, qx = q - qy * nqx;
-      const int qx0 = (bx0 + qx) * 8, qy0 = (by0 + qy) * 8;
-      uint64_t bits = rec.mask;
-      const double *w = pool + rec.offset;
-      while (bits) {
-        const int p = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        const double wv = *w++;
-        const int px = qx0 + (p & 7), py = qy0 + (p >> 3);
-        const int64_t pix = vbase + (int64_t)py * W + px;
-        if (!val[pix]) continue;  // invalid targets may be NaN: never read
-        const double u = (double)tgt[2 * pix], vv = (double)tgt[2 * pix + 1];
-        const double dx = (double)(px - ax), dy = (double)(py - ay);
-        const double ua = u - fax, va = vv - fay;
-        const double wx = wv * dx, wy = wv * dy;
-        m[0] += wv;
-        m[1] += wx;
-        m[2] += wy;
-        m[3] += wx * dx;
-        m[4] += wx * dy;
-        m[5] += wy * dy;
-        m[6] += wv * ua;
-        m[7] += wv * va;
-        m[8] += wx * ua;
-        m[9] += wx * va;
-        m[10] += wy * ua;
-        m[11] += wy * va;
-        const bool st = is_static(u, vv, px, py, static_thr);
-        m[12] += st ? wv : 0.0;
-        scnt += st;
-        cnt++;
-      }
-    }
-    fits[i] = solve_moments(m, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
-  }
-}
-
-void launch_k23_cached(const void *recs, const double *pool, const uint8_t *flag,
-                       const uint32_t *inst_base, const int16_t *bbox, const uint32_t *list,
-                       const uint32_t *n_list, int64_t n, int64_t nv_total, int W, int H,
-                       const void *tgt, int track_dtype, const uint8_t *val,
-                       const ts_config &cfg, ts_motions m, const uint8_t *touched,
-                       const uint32_t *rank, void *fits, cudaStream_t s) {
-  if (!nv_total) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks(nv_total, 256), (int64_t)sms * 8);
-  GvMotion *f = reinterpret_cast<GvMotion *>(fits);
-  const CacheRec *r = reinterpret_cast<const CacheRec *>(recs);
-  if (track_dtype == TS_TRACK_F32)
-    k23_cached<float><<<grid, 256, 0, s>>>(r, pool, flag, inst_base, bbox, list, n_list, n, W, H,
-                                           reinterpret_cast<const float *>(tgt), val,
-                                           cfg.static_threshold_px, cfg.det_floor,
-                                           cfg.min_pixels, cfg.min_weight, f);
-  else
-    k23_cached<double><<<grid, 256, 0, s>>>(r, pool, flag, inst_base, bbox, list, n_list, n, W, H,
-                                            reinterpret_cast<const double *>(tgt), val,
-                                            cfg.static_threshold_px, cfg.det_floor,
-                                            cfg.min_pixels, cfg.min_weight, f);
-  k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank, f, nv_total, m);
-}
-
 // solve_view on absolute moments (motion2d.py:164-184).
 __global__ void k_solve_abs(const double *__restrict__ v1, const double *__restrict__ v2,
                             const double *__restrict__ wsum, const int64_t *__restrict__ cnt,
@@ -367,6 +272,14 @@ __global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ se
 
 
 size_t k3_fit_bytes() { return sizeof(GvMotion); }
+
+void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
+                     int64_t nv_total, ts_motions m, cudaStream_t s) {
+  if (!nv_total) return;
+  k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank,
+                                                 reinterpret_cast<const GvMotion *>(fits),
+                                                 nv_total, m);
+}
 
 void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t *inst_base,
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,

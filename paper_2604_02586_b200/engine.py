@@ -193,6 +193,19 @@ class FrameEngine:
                       "ts_frame_cache")
         return self
 
+    def cache_info(self):
+        """(records, cached w values) of the current clip cache, summed over the plans."""
+        import ctypes
+        plans = [self.plan] if not self.grouped else [g[2] for g in self._groups]
+        tot = [0, 0]
+        for plan in plans:
+            r, v = ctypes.c_uint64(), ctypes.c_uint64()
+            nat.check(self._lib.ts_frame_cache_info(plan.handle, ctypes.byref(r), ctypes.byref(v)),
+                      "ts_frame_cache_info")
+            tot[0] += r.value
+            tot[1] += v.value
+        return tuple(tot)
+
     def drop_cache(self):
         plans = [self.plan] if not self.grouped else [g[2] for g in self._groups]
         for plan in plans:

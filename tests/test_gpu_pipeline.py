@@ -59,7 +59,10 @@ def test_frame_matches_compensate_frame(small_scene):
     tgt, val = oracle_tracks(s, 2)
     single = compensate_frame(s.frames[0], s.cameras, (tgt, val), frame_index=2)
     piped = run_pipeline(s, clip_len=9)[2]
-    np.testing.assert_array_equal(single.gaussians.rows, piped.gaussians.rows)
+    # run_pipeline applies frame 2's tracks to the clip's contribution cache (ts_frame_cache):
+    # the same contributions summed in another order, so equal to rounding, not bit for bit
+    np.testing.assert_allclose(single.gaussians.rows, piped.gaussians.rows, rtol=1e-11,
+                               atol=1e-14)
     assert single.tallies == piped.tallies
     assert sum(single.tallies.values()) == s.n_gaussians and single.compensated_from == 0
 
