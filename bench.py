@@ -63,6 +63,10 @@ HBM_FALLBACK = 6650.0
 # K3 split (touched list + scan + compact fits + merge, chosen from 16 M gvs on: cfg5) adds 5
 LAUNCHES_PER_STEP = 33
 LAUNCHES_K3_SPLIT = 5
+# clip mode with the contribution cache (profiles/r02_clip_launches_cfg{4,5}.txt: 222 launches
+# for two builds + 16 frames): binning + cache build 39, each cached frame 9
+LAUNCHES_CACHE_BUILD = 39
+LAUNCHES_CACHED_FRAME = 9
 
 
 def launches_per_step(n, nv):
@@ -308,7 +312,9 @@ def run_ours(args):
         if gather_bufs is not None and gather_ev[i] is not None:
             streams[i].wait_event(gather_ev[i])  # outs[i] was last read by a gather
         engs[i].bin(g_dev, cams, stream=streams[i])
-        outs[i] = engs[i].compensate(tgt, val, outs[i], stream=streams[i])
+        # the step's product is the updated Gaussians (FrameResult, pipeline.py:40-45); the
+        # per-view motions stay K3's intermediates
+        outs[i] = engs[i].compensate(tgt, val, outs[i], stream=streams[i], motions=False)
         return i
 
     for s_ in streams:
@@ -366,7 +372,7 @@ def run_ours(args):
     eng.plan.timing(True)
     for _ in range(min(args.steps, 20)):
         eng.bin(g_dev, cams)
-        out = eng.compensate(tgt, val, out)
+        out = eng.compensate(tgt, val, out, motions=False)
     torch.cuda.synchronize()
     stages = eng.plan.timing_read()
     eng.plan.timing(False)
@@ -559,7 +565,7 @@ def run_clip(args):
     stream = torch.cuda.current_stream()
     gather_stream = torch.cuda.Stream()
     eng.bin(g_dev, cams)
-    outs = {f: eng.alloc_outputs() for f in mine}
+    outs = {f: eng.alloc_outputs(motions=False) for f in mine}
     slots = max(len(frames_for_rank(targets, r, world)) for r in range(world))
     bufs = None
     if world > 1:
@@ -630,8 +636,11 @@ def run_clip(args):
                 "config": cfg, "frames_per_s": T / (ms / 1e3),
                 "parallelism": f"frame-sharded x{world} (strong: {T} frames per step)",
                 "frames_per_rank": [len(frames_for_rank(targets, r, world)) for r in range(world)],
-                # per step: one binning (21 launches) + per frame K2-K4 (12, +5 with the K3 split)
-                "gpu_launches": args.steps * (21 + len(mine) * (launches_per_step(n, nv) - 21)),
+                # per step: one binning (21 launches) + per frame K2-K4 (12, +5 with the K3
+                # split); with the cache: binning + build, then the cached frames
+                "gpu_launches": args.steps * (
+                    LAUNCHES_CACHE_BUILD + len(mine) * LAUNCHES_CACHED_FRAME if use_cache else
+                    21 + len(mine) * (launches_per_step(n, nv) - 21)),
                 "clocks": clk.summary()}
     if world > 1:
         dist.destroy_process_group()

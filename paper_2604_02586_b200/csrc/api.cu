@@ -625,7 +625,12 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   if (!m.pixel_count) m.pixel_count = im.pixel_count;
 
   const bool cached = p->cache_valid;
+  // no motions requested and K3's fits compact (cache or touched list): K4 reads the fits in
+  // place and only the statuses are written densely (the per-view motions are intermediates of
+  // compensate_frame, pipeline.py:117-124; FrameResult does not carry them)
+  bool compact = false;
   if (cached) {
+    compact = !motions && updates;
     // the clip's contribution cache: this frame's moments and fits straight from the cached
     // contributions (no rasterization, no partials); list, ranks and ranges set by ts_frame_cache
     uint32_t *list = ptr<uint32_t>(p->k3_list);
@@ -638,7 +643,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                                   ptr<double>(p->cache_scratch), s));
     p->mark_end(ST_RASTER, e3, s);
     cudaEvent_t e4 = p->mark_begin(s);
-    launch_k3_merge(ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, NV, m, s);
+    launch_k3_merge(ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, NV, m, s,
+                    compact);
     TS_CUDA_TRY(cudaGetLastError());
     p->mark_end(ST_SOLVE, e4, s);
   } else {
@@ -662,6 +668,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   p->k3_last_nv = NV;
   p->k3_last_split = split;
   const bool use_touched = split && k2_writes_touched();
+  compact = use_touched && !motions && updates;
   if (use_touched) {
     ENSURE(p->touched, NV + 8);
     ENSURE(p->k3_list, 4 * (NV + 8));
@@ -704,7 +711,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
                   use_touched ? ptr<uint32_t>(p->k3_list) : nullptr,
                   use_touched ? ptr<uint32_t>(p->k3_list) + NV + 4 : nullptr,
                   use_touched ? ptr<uint32_t>(p->k3_rank) : nullptr,
-                  use_touched ? p->k3_fits.p : nullptr, s);
+                  use_touched ? p->k3_fits.p : nullptr, s, compact);
   if (use_touched)  // touched count for the next frame's choice
     TS_CUDA_TRY(cudaMemcpyAsync(p->host_small + 8, ptr<uint32_t>(p->k3_list) + NV + 4, 4,
                                 cudaMemcpyDeviceToHost, s));
@@ -716,7 +723,8 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   ENSURE(p->k4_ws, k4_workspace_bytes(n));
   cudaEvent_t e5 = p->mark_begin(s);
   launch_k4_fuse(p->gaussians, n, ptr<ts_camera>(p->cams), p->V, m, p->cfg, *updates,
-                 p->k4_ws.p, s);
+                 p->k4_ws.p, s, compact ? p->k3_fits.p : nullptr,
+                 compact ? ptr<uint32_t>(p->k3_rank) : nullptr);
   TS_CUDA_TRY(cudaGetLastError());
   p->mark_end(ST_FUSE, e5, s);
   return TS_OK;

@@ -57,7 +57,7 @@ __device__ __forceinline__ void store_updates(ts_updates u, int64_t g, const dou
 // streaming QR loops over the solved views: mixed counts and early exits left ~12 of 32 lanes
 // active, and the heaviest warps last made a tail).
 __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int64_t n, int V,
-                                               ts_motions m, ts_config cfg, ts_updates u,
+                                               K4Motions m, ts_config cfg, ts_updates u,
                                                uint32_t *__restrict__ key,
                                                uint32_t *__restrict__ val,
                                                uint64_t *__restrict__ solved_mask) {
@@ -69,11 +69,14 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
   uint64_t mask = 0;
   for (int v = 0; v < V; v++) {
     const int64_t gv = (int64_t)v * n + g;
-    if (m.status[gv] != TS_STATUS_SOLVED) continue;
+    if (mot_status(m, gv) != TS_STATUS_SOLVED) continue;
     if (v < 64) mask |= 1ull << v;
     n_solved++;
-    tw += m.weight_sum[gv];
-    tp += m.pixel_count[gv];
+    double w;
+    int64_t c;
+    mot_sums(m, gv, w, c);
+    tw += w;
+    tp += c;
   }
   const bool ok = n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
                   tp >= cfg.min_total_pixels;
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(256) k4_prep(const double *__restrict__ G, int
 
 __global__ void __launch_bounds__(128, TS_K4_MIN_BLOCKS) k4_fuse(const double *__restrict__ G, int64_t n,
                                                const ts_camera *__restrict__ cams, int V,
-                                               ts_motions m, ts_config cfg, ts_updates u,
+                                               K4Motions m, ts_config cfg, ts_updates u,
                                                const uint32_t *__restrict__ order_key,
                                                const uint32_t *__restrict__ order,
                                                const uint64_t *__restrict__ solved_mask,
@@ -252,9 +255,11 @@ size_t k4_workspace_bytes(int64_t n) {
          align256(8 * (size_t)n) + align256(k4_sort_temp_bytes(n));
 }
 
-void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s) {
+void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions dense,
+                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s,
+                    const void *fits, const uint32_t *rank) {
   if (!n) return;
+  const K4Motions m{dense, reinterpret_cast<const GvMotion *>(fits), rank};
   char *ws = reinterpret_cast<char *>(workspace);
   unsigned *n_defer = reinterpret_cast<unsigned *>(ws);
   K4Deferred *defer = reinterpret_cast<K4Deferred *>(ws + 256);

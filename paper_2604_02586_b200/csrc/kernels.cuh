@@ -79,8 +79,9 @@ cudaError_t launch_k23_cached(const void *chunks, const uint32_t *counters, uint
                               const uint32_t *cxy, const void *track_target, int track_dtype,
                               const uint8_t *track_valid, const ts_config &cfg, void *fits,
                               double *scratch, cudaStream_t s);
+// status_only: only m.status is written (K4 then reads the compact fits)
 void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
-                     int64_t nv_total, ts_motions m, cudaStream_t s);
+                     int64_t nv_total, ts_motions m, cudaStream_t s, bool status_only = false);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
 bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched bytes
 
@@ -89,7 +90,7 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, const uint8_t *touched,
                      const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
-                     void *fits, cudaStream_t s);
+                     void *fits, cudaStream_t s, bool status_only = false);
 size_t k3_fit_bytes();  // per touched gv, the compact fit record of K3
 
 // solve_view on absolute moments (stage API)
@@ -107,8 +108,10 @@ void launch_accumulate(int64_t n, const uint32_t *seg_start, const uint32_t *seg
 
 // K4: multi-view fuse (update_all)
 size_t k4_workspace_bytes(int64_t n);
+// fits / rank != NULL: the per-view a, b and sums come from K3's compact fits (m.status dense)
 void launch_k4_fuse(const double *G, int64_t n, const ts_camera *cams, int V, ts_motions m,
-                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s);
+                    const ts_config &cfg, ts_updates u, void *workspace, cudaStream_t s,
+                    const void *fits = nullptr, const uint32_t *rank = nullptr);
 void launch_triangulate_batch(const double *rows, const int32_t *n_rows, int64_t batch,
                               int max_rows, double *x, int8_t *status, cudaStream_t s);
 void launch_cov3d_batch(const double *lin, const double *rhs, const int32_t *n_rows,

@@ -8,6 +8,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "motion.cuh"
 
 namespace ts {
 
@@ -559,14 +560,51 @@ TS_HD int fuse_finish(const double *gs, const double (&R4)[4][4], const double (
   return TS_STATUS_SOLVED;
 }
 
+// The per-view motion records K4 reads: the dense SoA arrays (ts_motions), or dense statuses plus
+// K3's compact list-order fits found through the gv's rank (K4Motions with fits != NULL: K3 kept
+// its fits compact, so the dense a / b / sums were never written; only SOLVED gvs are read, and
+// every SOLVED gv is in the touched list).
+struct K4Motions {
+  ts_motions m;
+  const GvMotion *fits;
+  const uint32_t *rank;
+};
+TS_HD int8_t mot_status(const ts_motions &m, int64_t gv) { return m.status[gv]; }
+TS_HD int8_t mot_status(const K4Motions &k, int64_t gv) { return k.m.status[gv]; }
+TS_HD void mot_sums(const ts_motions &m, int64_t gv, double &w, int64_t &c) {
+  w = m.weight_sum[gv];
+  c = m.pixel_count[gv];
+}
+TS_HD void mot_sums(const K4Motions &k, int64_t gv, double &w, int64_t &c) {
+  if (!k.fits) return mot_sums(k.m, gv, w, c);
+  const GvMotion &f = k.fits[k.rank[gv]];
+  w = f.wsum;
+  c = f.count;
+}
+TS_HD void mot_affine(const ts_motions &m, int64_t gv, double (&A)[4], double (&b)[2]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) A[i] = m.a[4 * gv + i];
+  b[0] = m.b[2 * gv];
+  b[1] = m.b[2 * gv + 1];
+}
+TS_HD void mot_affine(const K4Motions &k, int64_t gv, double (&A)[4], double (&b)[2]) {
+  if (!k.fits) return mot_affine(k.m, gv, A, b);
+  const GvMotion &f = k.fits[k.rank[gv]];
+#pragma unroll
+  for (int i = 0; i < 4; i++) A[i] = f.a[i];
+  b[0] = f.b[0];
+  b[1] = f.b[1];
+}
+
 // update_all for one Gaussian (multiview.py:181-274).  Reads the V per-view motion records of
 // Gaussian g (stride n between views) and writes its update; returns the status.
 // With allow_slow == false the SVD-deciding Gaussians return TS_FUSE_DEFER_STATUS and leave their
 // R factors in R4 / R6 / c6 for fuse_finish in the deferred pass.
 // `eligible_mask` != 0: the caller already applied the eligibility rule and passes the SOLVED-view
 // bits (k4_prep), so the per-view status / weight / count reads are not repeated.
+template <typename Motions>
 TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera *cams, int V,
-                        const ts_motions &m, const ts_config &cfg, double *delta, double *q,
+                        const Motions &m, const ts_config &cfg, double *delta, double *q,
                         double *sc, double (&R4)[4][4], double (&R6)[6][6], double (&c6)[6],
                         bool allow_slow, double *dbg = nullptr, uint64_t eligible_mask = 0) {
   double c3[9];
@@ -599,11 +637,14 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     int64_t tp = 0;
     for (int v = 0; v < V; v++) {
       const int64_t gv = (int64_t)v * n + g;
-      if (m.status[gv] != TS_STATUS_SOLVED) continue;
+      if (mot_status(m, gv) != TS_STATUS_SOLVED) continue;
       if (v < 64) solved |= 1ull << v;
       n_solved++;
-      tw += m.weight_sum[gv];
-      tp += m.pixel_count[gv];
+      double w;
+      int64_t c;
+      mot_sums(m, gv, w, c);
+      tw += w;
+      tp += c;
     }
     if (!(n_solved >= cfg.min_views && tw >= cfg.min_total_weight &&
           tp >= cfg.min_total_pixels))
@@ -617,7 +658,7 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     solved = 0;
     const int top = V - base < 64 ? V - base : 64;
     for (int j = 0; j < top; j++)
-      if (m.status[(int64_t)(base + j) * n + g] == TS_STATUS_SOLVED) solved |= 1ull << j;
+      if (mot_status(m, (int64_t)(base + j) * n + g) == TS_STATUS_SOLVED) solved |= 1ull << j;
    }
    while (solved && !bad) {
     const int v = base + ffs64_hd(solved) - 1;
@@ -626,9 +667,10 @@ TS_HD int fuse_gaussian(const double *gs, int64_t g, int64_t n, const ts_camera 
     const ts_camera &cam = cams[v];
     Projection p;
     project(gs, c3, cam, p);
-    const double A00 = m.a[4 * gv], A01 = m.a[4 * gv + 1], A10 = m.a[4 * gv + 2],
-                 A11 = m.a[4 * gv + 3];
-    const double b0 = m.b[2 * gv], b1 = m.b[2 * gv + 1];
+    double Av[4], bv[2];
+    mot_affine(m, gv, Av, bv);
+    const double A00 = Av[0], A01 = Av[1], A10 = Av[2], A11 = Av[3];
+    const double b0 = bv[0], b1 = bv[1];
     // Eq. 2: moved mean / covariance (multiview.py:218-220)
     const double mm0 = (A00 * p.mean2[0] + A01 * p.mean2[1]) + b0;
     const double mm1 = (A10 * p.mean2[0] + A11 * p.mean2[1]) + b1;

@@ -273,9 +273,24 @@ __global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ se
 
 size_t k3_fit_bytes() { return sizeof(GvMotion); }
 
+// The statuses alone (the compact fits stay where they are for K4): 2 bytes per gv.
+__global__ void __launch_bounds__(256) k3_merge_status(const uint8_t *__restrict__ touched,
+                                                       const uint32_t *__restrict__ rank,
+                                                       const GvMotion *__restrict__ fits,
+                                                       int64_t NV, int8_t *__restrict__ status) {
+  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gv >= NV) return;
+  status[gv] = touched[gv] ? fits[rank[gv]].status : (int8_t)TS_STATUS_UNSOLVABLE;
+}
+
 void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
-                     int64_t nv_total, ts_motions m, cudaStream_t s) {
+                     int64_t nv_total, ts_motions m, cudaStream_t s, bool status_only) {
   if (!nv_total) return;
+  if (status_only) {
+    k3_merge_status<<<blocks(nv_total, 256), 256, 0, s>>>(
+        touched, rank, reinterpret_cast<const GvMotion *>(fits), nv_total, m.status);
+    return;
+  }
   k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank,
                                                  reinterpret_cast<const GvMotion *>(fits),
                                                  nv_total, m);
@@ -285,7 +300,7 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
                      const uint32_t *ntiles, const int16_t *bbox, int64_t nv_total,
                      const ts_config &cfg, ts_motions m, const uint8_t *touched,
                      const uint32_t *list, const uint32_t *n_list, const uint32_t *rank,
-                     void *fits, cudaStream_t s) {
+                     void *fits, cudaStream_t s, bool status_only) {
   if (!nv_total) return;
   if (!touched) {  // every gv walks its flags
     k3_solve<<<blocks(nv_total, 256), 256, 0, s>>>(partial, flag, inst_base, ntiles, bbox, nv_total,
@@ -300,7 +315,7 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
   GvMotion *f = reinterpret_cast<GvMotion *>(fits);
   k3_solve_list<<<(unsigned)grid, 256, 0, s>>>(partial, flag, inst_base, bbox, list, n_list,
                                                cfg.det_floor, cfg.min_pixels, cfg.min_weight, f);
-  k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank, f, nv_total, m);
+  launch_k3_merge(touched, rank, f, nv_total, m, s, status_only);
 }
 
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,

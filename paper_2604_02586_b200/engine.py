@@ -246,11 +246,23 @@ class FrameEngine:
         return total
 
     # -- K2 + K3 + K4 ----------------------------------------------------------------------
-    def alloc_outputs(self):
+    MOTION_FIELDS = ("motion_status", "motion_a", "motion_b", "weight_sum", "pixel_count",
+                     "static_pixel_count", "static_weight_sum")
+
+    def alloc_outputs(self, motions=True):
+        """Output buffers of compensate().  motions=False: the updates only -- the per-view
+        motions are intermediates of compensate_frame (pipeline.py:117-124; FrameResult carries
+        the updated Gaussians), so K3 may keep its fits compact and K4 read them in place."""
         torch = _torch()
         n, nv = self.n, self.n * self.n_views
         dev = self._gauss.device
         f64 = dict(dtype=torch.float64, device=dev)
+        if not motions:
+            return FrameOutputs(
+                delta_mean=torch.empty((n, 3), **f64), rotation=torch.empty((n, 4), **f64),
+                scale=torch.empty((n, 3), **f64),
+                status=torch.empty(n, dtype=torch.int8, device=dev),
+                **{k: None for k in self.MOTION_FIELDS})
         return FrameOutputs(
             delta_mean=torch.empty((n, 3), **f64), rotation=torch.empty((n, 4), **f64),
             scale=torch.empty((n, 3), **f64), status=torch.empty(n, dtype=torch.int8, device=dev),
@@ -269,9 +281,12 @@ class FrameEngine:
                     motion_status=(nv,), motion_a=(nv, 2, 2), motion_b=(nv, 2),
                     weight_sum=(nv,), pixel_count=(nv,), static_pixel_count=(nv,),
                     static_weight_sum=(nv,))
+        no_motions = all(getattr(out, k) is None for k in self.MOTION_FIELDS)
         for k, shape in want.items():
             t = getattr(out, k)
-            if tuple(t.shape) != shape or t.device != dev or not t.is_contiguous():
+            if t is None and no_motions and k in self.MOTION_FIELDS:
+                continue
+            if t is None or tuple(t.shape) != shape or t.device != dev or not t.is_contiguous():
                 return False
         return True
 
@@ -282,7 +297,7 @@ class FrameEngine:
                              f"(N={self.n}, views={self.n_views}); use alloc_outputs()")
 
     def compensate(self, track_target, track_valid, out: FrameOutputs | None = None,
-                   stream=None) -> FrameOutputs:
+                   stream=None, motions=True) -> FrameOutputs:
         """Fused raster-accumulate, per-view affine fit and multi-view fuse for one frame.
 
         Tracks: (V, H, W, 2) targets and (V, H, W) validity (device tensors, pinned host tensors
@@ -292,7 +307,7 @@ class FrameEngine:
         if self._gauss is None:
             raise RuntimeError("FrameEngine.bin() must run before compensate()")
         if self.grouped or isinstance(track_target, (list, tuple)):
-            return self._compensate_groups(track_target, track_valid, out, stream)
+            return self._compensate_groups(track_target, track_valid, out, stream, motions)
         tgt, val = track_target, track_valid
         # each array: a CUDA tensor as is; a pinned CPU tensor is read in place by K2 (zero-copy:
         # only the occupied tiles' quadrants cross PCIe); anything else is copied to the device
@@ -318,17 +333,20 @@ class FrameEngine:
                                     f"match {expect}")
         dtype = nat.TS_TRACK_F32 if tgt.dtype == torch.float32 else nat.TS_TRACK_F64
         if out is None:
-            out = self.alloc_outputs()
+            out = self.alloc_outputs(motions)
         else:
             self.check_outputs(out)
-        m = nat.Motions(nat.dptr(out.motion_status).value, nat.dptr(out.motion_a).value,
-                        nat.dptr(out.motion_b).value, nat.dptr(out.weight_sum).value,
-                        nat.dptr(out.pixel_count).value, nat.dptr(out.static_pixel_count).value,
-                        nat.dptr(out.static_weight_sum).value)
+        m = None
+        if out.motion_status is not None:
+            m = ctypes.byref(nat.Motions(
+                nat.dptr(out.motion_status).value, nat.dptr(out.motion_a).value,
+                nat.dptr(out.motion_b).value, nat.dptr(out.weight_sum).value,
+                nat.dptr(out.pixel_count).value, nat.dptr(out.static_pixel_count).value,
+                nat.dptr(out.static_weight_sum).value))
         u = nat.Updates(nat.dptr(out.delta_mean).value, nat.dptr(out.rotation).value,
                         nat.dptr(out.scale).value, nat.dptr(out.status).value)
         nat.check(self._lib.ts_frame_compensate(self.plan.handle, nat.dptr(tgt), dtype,
-                                                nat.dptr(val), ctypes.byref(m), ctypes.byref(u),
+                                                nat.dptr(val), m, ctypes.byref(u),
                                                 nat.stream_ptr(stream)), "ts_frame_compensate")
         return out
 
@@ -352,7 +370,7 @@ class FrameEngine:
             val = as_device(val, torch.uint8)
         return tgt, val
 
-    def _compensate_groups(self, targets, valids, out, stream):
+    def _compensate_groups(self, targets, valids, out, stream, motions=True):
         """Per-view track lists, and rigs binned as several plans: K2+K3 per plan into the
         plan's slice of the view-major motion arrays, then K4 over every view."""
         torch = _torch()
@@ -368,9 +386,14 @@ class FrameEngine:
                                         f"{tuple(val.shape)} vs camera {w}x{h}")
             tv.append((tgt, val))
         if out is None:
-            out = self.alloc_outputs()
+            out = self.alloc_outputs(motions)
         else:
             self.check_outputs(out)
+        if out.motion_status is None:  # the fuse over all views reads the dense motions
+            full = self.alloc_outputs()
+            for k in ("delta_mean", "rotation", "scale", "status"):
+                setattr(full, k, getattr(out, k))
+            out = full
         groups = self._groups or [(0, self.n_views, self.plan)]
         n = self.n
         for v0, v1, plan in groups:
@@ -550,7 +573,8 @@ class StreamingEngine:
             if self._out_free[e] is not None:
                 self._out_free[e].synchronize()  # shapes changed: reallocate after the last D2H
             self._outs[e] = None
-        out = eng.compensate(t_d, v_d, self._outs[e], stream=cs)
+        # the host result is the updated Gaussians: no per-view motions (K4 reads K3's fits)
+        out = eng.compensate(t_d, v_d, self._outs[e], stream=cs, motions=False)
         self._outs[e] = out
         computed = torch.cuda.Event(enable_timing=True)
         computed.record(cs)

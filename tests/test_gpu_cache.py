@@ -93,3 +93,24 @@ def test_cache_at_scale_cfg3():
         got = eng.compensate(tgt, val)
         torch.cuda.synchronize()
         _compare(ref, got, n, nv)
+
+
+@pytest.mark.parametrize("use_cache", [False, True])
+def test_compact_fits_same_updates(use_cache):
+    """motions=False: K3 keeps its fits compact (cache / touched list) and K4 reads them in place
+    (only the statuses are written densely) -- the updates must equal the dense path's bit for
+    bit, since K4 reads the same numbers."""
+    _need_cuda()
+    from paper_2604_02586_b200.engine import FrameEngine
+    d = gd.load("scene21")
+    target, valid = gd.tracks(d)
+    eng = FrameEngine().bin(d["gaussians"], d["cameras"])
+    if use_cache:
+        eng.build_cache()
+    t, v = _tracks(target, valid, 0.4)
+    a = eng.compensate(t, v)
+    b = eng.compensate(t, v, motions=False)
+    torch.cuda.synchronize()
+    assert b.motion_status is None
+    for k in ("delta_mean", "rotation", "scale", "status"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k

@@ -24,6 +24,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--frames", type=int, default=8)
+    ap.add_argument("--passes", default="0,1,1",
+                    help="cache off (0) / on (1) per pass; the second cached pass runs on sized buffers")
     args = ap.parse_args()
     c = bench.CONFIGS[args.config]
     frames = [c["gap"] * (j + 1) for j in range(args.frames)]
@@ -32,7 +34,7 @@ def main():
     eng = FrameEngine()
     eng.bin(g, scene.cameras)
     outs = {f: eng.compensate(*tracks[f]) for f in frames}  # warm-up, allocations
-    for use_cache in (False, True, True):  # the second cached pass: buffers already sized
+    for use_cache in [p == "1" for p in args.passes.split(",")]:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         torch.cuda.nvtx.range_push("build")

@@ -40,5 +40,21 @@ done
 timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "frame/" -k regex:k2_raster \
   --launch-skip 1 --launch-count 1 -o $O/k2_cfg2 -f python tools/profile_frame.py --config cfg2 --frames 3 > $O/ncu_k2_cfg2.log 2>&1
 fi
+if [ $STAGE = all -o $STAGE = clip ]; then
+# clip mode with the contribution cache: launch list of cache builds ("build") and cached frames
+# ("frame"), and one --set full capture of a cached cfg5 frame
+for c in ${CLIP_CFGS:-cfg4 cfg5}; do
+  timeout 600 ncu --nvtx --nvtx-include "build/" --nvtx-include "frame/" --metrics gpu__time_duration.sum \
+    --clock-control none --csv --log-file $O/clip_launches_$c.csv python tools/cache_timing.py --config $c \
+    --frames 8 --passes 1,1 > $O/ncu_clip_launch_$c.log 2>&1
+  python tools/summarize_ncu.py launches $O/clip_launches_$c.csv > $O/clip_launches_$c.txt 2>&1
+done
+timeout 900 ncu --set full --clock-control none --nvtx --nvtx-include "frame/" -k regex:"k23_cached|k3_merge|k4_fuse" --launch-skip 6 --launch-count 4 \
+  -o /tmp/clip_cfg5 -f python tools/cache_timing.py --config cfg5 --frames 8 --passes 1,1 > $O/ncu_clip_full_cfg5.log 2>&1
+python tools/summarize_ncu.py report /tmp/clip_cfg5.ncu-rep > $O/clip_kernels_cfg5.txt 2>&1
+timeout 900 python bench.py --config cfg5 --clip-frames 8 --steps 3 --warmup 3 > $O/bench_cfg5_clip8.json 2> $O/bench_cfg5_clip8.err
+timeout 900 python bench.py --config cfg4 --clip-frames 8 --steps 5 --warmup 3 > $O/bench_cfg4_clip8.json 2> $O/bench_cfg4_clip8.err
+timeout 900 python bench.py --config cfg5 --clip-frames 8 --no-cache --steps 3 --warmup 3 > $O/bench_cfg5_clip8_nocache.json 2> $O/bench_cfg5_clip8_nocache.err
+fi
 du -sh $O
 echo done
