@@ -126,8 +126,11 @@ int ts_frame_bin(ts_plan *plan, const double *gaussians, int64_t n, const ts_cam
  * host arrays in place over PCIe (zero-copy), only the 8x8 quadrants of occupied tiles -- about
  * a tenth of the pixels at the benchmark configs; the host must not modify them until the
  * frame's work on `stream` completes.  Pageable host memory: TS_E_INVALID_ARGUMENT.
- * motions may have NULL members (then only the internal copy is kept).  updates == NULL stops
- * after K3 (the per-view motions of a view group; motions must then be non-NULL). */
+ * motions may have NULL members (then only the internal copy is kept); motions == NULL (the
+ * per-view motions are intermediates: the reference's FrameResult carries only the updates)
+ * lets K4 read K3's compact fits in place when K3 ran over its touched-gv list or the clip
+ * cache.  updates == NULL stops after K3 (the per-view motions of a view group; motions must
+ * then be non-NULL). */
 int ts_frame_compensate(ts_plan *plan, const void *track_target, int32_t track_dtype,
                         const uint8_t *track_valid, const ts_motions *motions,
                         const ts_updates *updates, void *stream);
@@ -154,7 +157,8 @@ int ts_frame_occupied_tiles(const ts_plan *plan, int64_t *out);
 /* Clip contribution cache (enable = 1): runs K2 once over the current binning WITHOUT tracks and
  * keeps every kept contribution (pixel, w = alpha T) as one record per (Gaussian-view, 8x8
  * quadrant) in the plan; until the next ts_frame_bin (or enable = 0), ts_frame_compensate then
- * skips the rasterization and turns each record into its moments with the target frame's tracks
+ * skips the rasterization and forms each Gaussian-view's moments and fit from its cached
+ * contributions with the target frame's tracks
  * -- the GPU form of the reference's frame-0 weight-map reuse across a clip's target frames
  * (pipeline.py:191-196; compensate_frame(weightmaps=...), pipeline.py:110-116).
  * Synchronous (sizes the pool); TS_E_CAPACITY if the pool cannot be sized. */
