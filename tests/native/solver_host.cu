@@ -73,3 +73,15 @@ extern "C" void host_matmul3(const double *a, const double *b, double *c) { ts::
 extern "C" void host_matmul3_bt(const double *a, const double *b, double *c) {
   ts::matmul3_bt(a, b, c);
 }
+
+// the static test with and without the square root (cache.cu uses the latter)
+extern "C" double host_static_sq_limit(double thr) { return ts::static_sq_limit(thr); }
+extern "C" void host_static_both(const double *u, const double *v, const int32_t *px,
+                                 const int32_t *py, int64_t m, double thr, uint8_t *a,
+                                 uint8_t *b) {
+  const double lim = ts::static_sq_limit(thr);
+  for (int64_t i = 0; i < m; i++) {
+    a[i] = ts::is_static(u[i], v[i], px[i], py[i], thr);
+    b[i] = ts::is_static_sq(u[i], v[i], px[i], py[i], lim);
+  }
+}

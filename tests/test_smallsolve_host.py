@@ -90,3 +90,29 @@ def test_update_all_host(lib, scene):
     ang = 2 * np.arccos(np.clip(np.abs((q * d["u_rot"]).sum(1)), 0, 1))
     assert ang[ok].max() < 1e-6
     np.testing.assert_allclose(s[ok], d["u_scale"][ok], rtol=1e-10)
+
+
+@pytest.mark.parametrize("thr", [1.0, 0.5, 2.75, 1e-3, 0.0, -1.0, float("inf"), float("nan")])
+def test_static_without_sqrt(lib, thr):
+    """sqrt_rn(d0^2 + d1^2) < thr  <=>  d0^2 + d1^2 <= L(thr) (csrc/common.cuh): exact for every
+    input, including points on and one ulp around the threshold circle and non-finite tracks."""
+    lib.host_static_sq_limit.restype = ctypes.c_double
+    lib.host_static_sq_limit.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(7)
+    m = 200_000
+    px = rng.integers(0, 2000, m).astype(np.int32)
+    py = rng.integers(0, 2000, m).astype(np.int32)
+    t = thr if np.isfinite(thr) and thr > 0 else 1.0
+    ang = rng.uniform(0, 2 * np.pi, m)
+    rad = t * (1 + rng.choice([-1, 0, 1], m) * np.ldexp(1.0, -52) * rng.integers(0, 4, m))
+    rad[: m // 4] = rng.uniform(0, 3 * t, m // 4)
+    u = px + rad * np.cos(ang)
+    v = py + rad * np.sin(ang)
+    u[:50], v[50:100] = np.nan, np.inf
+    a = np.zeros(m, np.uint8)
+    b = np.zeros(m, np.uint8)
+    lib.host_static_both(_ptr(u), _ptr(v), _ptr(px), _ptr(py), ctypes.c_int64(m),
+                         ctypes.c_double(thr), _ptr(a), _ptr(b))
+    np.testing.assert_array_equal(a, b)
+    if np.isfinite(thr) and thr > 0:
+        assert 0 < a.sum() < m
