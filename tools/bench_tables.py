@@ -34,7 +34,7 @@ def main():
                     f"({e['zero_copy']['ms_per_step']:.2f} / {e['full_copy']['ms_per_step']:.2f}) | "
                     f"{e['value'] / 1e9:.2f} | {rf['kernel_ms']:.2f} | {rf['frac']:.3f} | "
                     f"{(rf['traffic'] or 0) / max(rf['algorithmic_bytes'], 1):.1f} |")
-    print("| cfg | workload | ms/step resident | G GV/s | e2e ms auto (in place / copy) | e2e G GV/s "
+    print("| cfg | workload | ms/step resident | G GV/s | e2e ms headline (in place / whole copy) | e2e G GV/s "
           "| K2 ms | K2 HBM frac | K2 traffic / algorithmic |")
     print("|---|---|---|---|---|---|---|---|---|")
     print("\n".join(rows))
