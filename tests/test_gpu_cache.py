@@ -114,3 +114,63 @@ def test_compact_fits_same_updates(use_cache):
     assert b.motion_status is None
     for k in ("delta_mean", "rotation", "scale", "status"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_cache_long_runs_and_f64_tracks():
+    """Large Gaussians (runs of far more than 128 cached contributions: the chunked per-frame
+    kernel's scratch reduction, k23_cached_multi) and float64 tracks (the double instantiation):
+    cached == per-frame to rounding, and the oracle's counts exactly."""
+    _need_cuda()
+    from paper_2604_02586_b200.engine import FrameEngine
+    from paper_2604_02586_b200.scene import generate_scene, oracle_tracks
+    scene = generate_scene(3, 400, 6, 3, focal=300, width=320, height=240,
+                           scale_range=(0.03, 0.12))
+    g, cams = scene.frames[0], scene.cameras
+    n, nv = len(g), len(cams)
+    plain = FrameEngine().bin(g, cams)
+    cached = FrameEngine().bin(g, cams).build_cache()
+    nrec, nw = cached.cache_info()
+    assert nrec > 0 and nw > 0
+    tgt, val = oracle_tracks(scene, 2, engine=plain)
+    tgt64 = tgt.to(torch.float64)
+    for t in (tgt, tgt64):
+        a = plain.compensate(t, val)
+        b = cached.compensate(t, val)
+        torch.cuda.synchronize()
+        _compare(a, b, n, nv)
+    # some gv has a run longer than one 128-contribution chunk
+    assert int(b.pixel_count.max()) > 128
+    rows = np.array([c.as_row() for c in cams])
+    upd, mots, accs = oracle.compensate(g, rows, list(tgt64.cpu().numpy()),
+                                        list(val.cpu().numpy().astype(bool)))
+    np.testing.assert_array_equal(b.pixel_count.cpu().numpy().reshape(nv, n),
+                                  np.stack([x["pixel_count"] for x in accs]))
+
+
+def test_cache_grouped_rig():
+    """Mixed image sizes (one plan per same-size group): every plan builds its cache."""
+    _need_cuda()
+    from paper_2604_02586_b200.engine import FrameEngine
+    d = gd.load("scene7")
+    target, valid = gd.tracks(d)
+    g = d["gaussians"]
+    cams = d["cameras"].copy()
+    targets, valids = [], []
+    for v in range(len(cams)):
+        if 3 <= v <= 5:
+            cams[v, 16], cams[v, 17] = 800, 500
+            targets.append(np.ascontiguousarray(target[v, :500, :800]).astype(np.float32))
+            valids.append(np.ascontiguousarray(valid[v, :500, :800]).astype(np.uint8))
+        else:
+            targets.append(target[v].astype(np.float32))
+            valids.append(valid[v].astype(np.uint8))
+    plain = FrameEngine().bin(g, cams)
+    cached = FrameEngine().bin(g, cams).build_cache()
+    assert cached.grouped
+    a = plain.compensate(targets, valids)
+    b = cached.compensate(targets, valids)
+    c = cached.compensate(targets, valids, motions=False)
+    torch.cuda.synchronize()
+    _compare(a, b, len(g), len(cams))
+    for k in ("delta_mean", "rotation", "scale", "status"):
+        assert torch.equal(getattr(b, k), getattr(c, k)), k
