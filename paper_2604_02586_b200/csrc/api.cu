@@ -767,8 +767,6 @@ int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
     TS_CUDA_TRY(cudaMemsetAsync(p->flag.p, 0, ns + 8, s));
     TS_CUDA_TRY(cudaMemsetAsync(p->touched.p, 0, NV + 8, s));
     TS_CUDA_TRY(cudaMemsetAsync(cur, 0, 16, s));
-    // reserved records no warp fills stay mask 0 (skipped per frame)
-    TS_CUDA_TRY(cudaMemsetAsync(p->cache_recs.p, 0, sizeof(CacheRec) * p->cache_rec_cap, s));
     TS_CUDA_TRY(launch_k2(K2_CACHE, TS_TRACK_F32, ptr<RasterRec>(p->rec), ptr<uint32_t>(p->tval2),
                           ptr<uint32_t>(p->range), ptr<uint32_t>(p->inst_base),
                           ptr<uint32_t>(p->items), ptr<uint32_t>(p->counters), 0,
@@ -813,14 +811,15 @@ int ts_frame_cache(ts_plan *p, int32_t enable, void *stream) {
   ENSURE(p->cache_ranges, 8 * (NV + 1));
   TS_CUDA_TRY(cudaMemsetAsync(p->cache_cnt.p, 0, 4 * (ns + 1), s));
   launch_cache_slot_counts(ptr<CacheRec>(p->cache_recs), cur + 1, p->cache_rec_cap,
-                           ptr<uint32_t>(p->cache_cnt), s);
+                           ptr<uint32_t>(p->cache_cnt), s, p->cache_recs_used);
   TS_CUDA_TRY(cub_call(p, s, [&](void *tmp, size_t &bytes) {
     return cub::DeviceScan::ExclusiveSum(tmp, bytes, ptr<uint32_t>(p->cache_cnt),
                                          ptr<uint32_t>(p->cache_off), (int)(ns + 1), s);
   }));
   launch_cache_scatter(ptr<CacheRec>(p->cache_recs), cur + 1, p->cache_rec_cap,
                        ptr<double>(p->cache_pool), ptr<uint32_t>(p->cache_off),
-                       ptr<double>(p->cache_w), ptr<uint32_t>(p->cache_xy), s);
+                       ptr<double>(p->cache_w), ptr<uint32_t>(p->cache_xy), s,
+                       p->cache_recs_used);
   launch_cache_ranges(list, n_list, NV, ptr<int16_t>(p->bbox), ptr<uint32_t>(p->inst_base),
                       ptr<uint32_t>(p->cache_off), ptr<uint2>(p->cache_ranges), s);
   // the per-frame work units: every gv's run cut into chunks of at most cache_chunk_len()

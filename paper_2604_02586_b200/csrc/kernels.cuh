@@ -56,10 +56,11 @@ cudaError_t launch_k2(int mode, int track_dtype, const RasterRec *rec, const uin
 // Clip cache (cache.cu): records -> contributions in slot order (cw, cxy) and per-gv ranges over
 // the touched list, once per clip; per target frame the moments + fits of the listed gvs.
 void launch_cache_slot_counts(const CacheRec *recs, const unsigned long long *n_recs,
-                              uint64_t rec_cap, uint32_t *slot_cnt, cudaStream_t s);
+                              uint64_t rec_cap, uint32_t *slot_cnt, cudaStream_t s,
+                              uint64_t n_hint);
 void launch_cache_scatter(const CacheRec *recs, const unsigned long long *n_recs, uint64_t rec_cap,
                           const double *pool, const uint32_t *slot_off, double *cw, uint32_t *cxy,
-                          cudaStream_t s);
+                          cudaStream_t s, uint64_t n_hint);
 void launch_cache_ranges(const uint32_t *list, const uint32_t *n_list, int64_t nv_total,
                          const int16_t *bbox, const uint32_t *inst_base, const uint32_t *slot_off,
                          uint2 *ranges, cudaStream_t s);

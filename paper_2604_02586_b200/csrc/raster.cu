@@ -219,6 +219,14 @@ struct CacheChunks {
   unsigned long long pool_cur = 0, pool_lim = 0, rec_cur = 0, rec_lim = 0;
 };
 
+// The unused tail of a warp's record chunk (abandoned for a fresh chunk, or left at exit) gets
+// mask 0, which the per-clip layout skips: no memset of the whole record array per build.
+__device__ __forceinline__ void k2_cache_clear_tail(const K2Params &P, int lane,
+                                                    const CacheChunks &ch) {
+  const unsigned long long lim = min(ch.rec_lim, (unsigned long long)P.rec_cap);
+  for (unsigned long long r = ch.rec_cur + lane; r < lim; r += 32) P.recs[r].mask = 0ull;
+}
+
 template <typename TrackT>
 __device__ __forceinline__ void k2_flush_cache(const K2Warp<TrackT> &S, const K2Params &P,
                                                int lane, int kcount, uint64_t my_cm,
@@ -246,6 +254,7 @@ __device__ __forceinline__ void k2_flush_cache(const K2Warp<TrackT> &S, const K2
     ch.pool_lim = ch.pool_cur + K2_CACHE_CHUNK;
   }
   if (ch.rec_cur + rtotal > ch.rec_lim) {
+    k2_cache_clear_tail(P, lane, ch);
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(P.rec_cursor, (unsigned long long)K2_CACHE_RECS);
     ch.rec_cur = __shfl_sync(0xffffffffu, base, 0);
@@ -514,6 +523,7 @@ __global__ void __launch_bounds__(K2_WARPS * 32, TS_K2_MIN_BLOCKS) k2_raster(con
       }
     }
   }
+  if (MODE == K2_CACHE) k2_cache_clear_tail(P, lane, cache_ch);
   if (K2_STATS_ON && lane == 0)
     for (int i = 0; i < K2S_N; i++) atomicAdd(&P.stats[i], st[i]);
 }
