@@ -16,6 +16,8 @@
 //      the global id) then groups every tile position tile-major, views in order, each
 //      (view, tile) list depth-ordered.
 //   4. k1_tile_ranges marks [start, end) of every (view, tile).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -102,7 +104,28 @@ __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__
     rx1 = max(rx1, __shfl_xor_sync(0xffffffffu, rx1, d));
     ry1 = max(ry1, __shfl_xor_sync(0xffffffffu, ry1, d));
   }
+  // the block's warps combine in shared memory: six atomics per block
+  __shared__ uint32_t s_lo[32], s_hi[32];
+  __shared__ int s_r[4][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    s_lo[w] = lo;
+    s_hi[w] = hi;
+    s_r[0][w] = rx0;
+    s_r[1][w] = ry0;
+    s_r[2][w] = rx1;
+    s_r[3][w] = ry1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < nw; k++) {
+      lo = min(lo, s_lo[k]);
+      hi = max(hi, s_hi[k]);
+      rx0 = min(rx0, s_r[0][k]);
+      ry0 = min(ry0, s_r[1][k]);
+      rx1 = max(rx1, s_r[2][k]);
+      ry1 = max(ry1, s_r[3][k]);
+    }
     if (lo != 0xFFFFFFFFu) atomicMin(&drange[2 * v], lo);
     if (hi != 0u) atomicMax(&drange[2 * v + 1], hi);
     if (rx1 >= 0) {
@@ -312,7 +335,10 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
   k1_range_init<<<1, 64, 0, s>>>(drange, V);
   k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, drange, dval,
                                                                   depth64, ntiles, status, bbox);
-  k1_depth_range<<<dim3(16, V), 256, 0, s>>>(depth64, status, bbox, n, drange);
+  // enough blocks per view that each thread reads ~8 gvs (16 per view was latency-bound at
+  // cfg5: 0.41 ms for 48 M gvs)
+  const int per_view = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (n + 2047) / 2048));
+  k1_depth_range<<<dim3(per_view, V), 256, 0, s>>>(depth64, status, bbox, n, drange);
   k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dbits, dkey);
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
