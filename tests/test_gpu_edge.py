@@ -186,3 +186,24 @@ def test_empty_frame(scene7):
     torch.cuda.synchronize()
     assert out.status.numel() == 0 and out.motion_status.numel() == 0
     assert out.tallies() == {"solved": 0, "static": 0, "unsolvable": 0}
+
+
+def test_cache_edge_cases(scene7):
+    """The clip contribution cache with no Gaussians, and with every track invalid (every cached
+    contribution dropped per frame: all UNSOLVABLE, frame-1 rotation / scale kept)."""
+    from paper_2604_02586_b200.engine import FrameEngine
+    g, cams, target, valid = scene7
+    eng = FrameEngine().bin(np.zeros((0, 11)), cams).build_cache()
+    out = eng.compensate(target.astype(np.float32), valid.astype(np.uint8), motions=False)
+    torch.cuda.synchronize()
+    assert out.status.numel() == 0 and eng.cache_info() == (0, 0)
+    eng = FrameEngine().bin(g, cams).build_cache()
+    assert eng.cache_info()[1] > 0
+    for motions in (True, False):
+        out = eng.compensate(target.astype(np.float32), np.zeros_like(valid, dtype=np.uint8),
+                             motions=motions)
+        torch.cuda.synchronize()
+        assert bool((out.status == 0).all())
+        np.testing.assert_array_equal(out.rotation.cpu().numpy(), g[:, 3:7])
+        if motions:
+            assert int(out.pixel_count.sum()) == 0 and bool((out.motion_status == 0).all())
