@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--full-copy", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["rect", "inplace", "copy", "auto"],
+                    help="track mode (overrides --full-copy)")
     args = ap.parse_args()
     c = bench.CONFIGS[args.config]
     scene, tracks = bench.make_inputs(args.config, c["gap"] + 1)
@@ -34,7 +36,9 @@ def main():
     t_hosts = [tgt.cpu().pin_memory() for _ in range(2)]
     v_hosts = [val.cpu().pin_memory() for _ in range(2)]
     res_host = E.StreamingEngine.result_buffer(len(scene.frames[0]))
-    st = E.StreamingEngine(zero_copy_tracks=not args.full_copy)
+    mode = {"rect": "rect", "inplace": True, "copy": False, "auto": "auto"}.get(
+        args.mode, not args.full_copy)
+    st = E.StreamingEngine(zero_copy_tracks=mode)
     marks = []  # (step, name, start_event, end_event)
     base = torch.cuda.Event(enable_timing=True)
 
@@ -82,6 +86,8 @@ def main():
               f"  ({a.elapsed_time(b):6.3f} ms)")
     for k, a, b in host:
         print(f"host step() call {k}: {a:8.3f} -> {b:8.3f} ms (wall)")
+    print(f"GPU: {base.elapsed_time(marks[-1][3]) / max(args.steps, 1):.3f} ms per step over the "
+          f"run; host: {host[-1][2] / max(args.steps, 1):.3f} ms per step() call")
 
 
 if __name__ == "__main__":
