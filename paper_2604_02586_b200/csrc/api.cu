@@ -72,8 +72,11 @@ struct ts_plan {
       inst_base, tkey, tkey2, tval, tval2, range, items, counters, cub_tmp;
   // per-frame state
   DevBuf k2_stats;
-  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, cache_pool, cache_cursor, cache_recs, cache_cnt, cache_off, cache_w, cache_xy, cache_ranges, cache_chunks, cache_multi, cache_scratch, cache_counters, mot_status, mot_a, mot_b, mot_w, mot_cnt, mot_scnt,
-      mot_sw;
+  DevBuf partial, flag, touched, k3_list, k3_rank, k3_fits, mot_status, mot_a, mot_b, mot_w,
+      mot_cnt, mot_scnt, mot_sw;
+  // clip contribution cache (ts_frame_cache, cache.cu)
+  DevBuf cache_pool, cache_cursor, cache_recs, cache_cnt, cache_off, cache_w, cache_xy,
+      cache_ranges, cache_chunks, cache_multi, cache_scratch, cache_counters;
   // stage-API buffers
   DevBuf emit_count, emit_key, emit_key2, emit_gv, emit_alpha, emit_trans, emit_idx, emit_idx2,
       deg_flags, deg_ids, deg_count, acc_keys, acc_keys2, acc_order, acc_iota, seg_start, seg_end;
@@ -145,7 +148,10 @@ int64_t sum_workspace(const ts_plan *p) {
                           &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi, &p->reg_static,
                           &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                           &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                          &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs, &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy, &p->cache_ranges, &p->cache_chunks, &p->cache_multi, &p->cache_scratch, &p->cache_counters};
+                          &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs,
+                          &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy,
+                          &p->cache_ranges, &p->cache_chunks, &p->cache_multi,
+                          &p->cache_scratch, &p->cache_counters};
   int64_t t = 0;
   for (const DevBuf *b : bufs) t += (int64_t)b->bytes;
   return t;
@@ -164,7 +170,9 @@ void release_all(ts_plan *p) {
                     &p->knn_val, &p->knn_val2, &p->knn_sp, &p->knn_lo, &p->knn_hi,
                     &p->reg_static, &p->reg_source, &p->reg_euler, &p->k4_ws, &p->drange, &p->k2_sched,
                     &p->touched, &p->k3_list, &p->k3_rank, &p->k3_fits, &p->tie_runs,
-                    &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs, &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy, &p->cache_ranges, &p->cache_chunks, &p->cache_multi, &p->cache_scratch, &p->cache_counters};
+                    &p->tie_tmp, &p->cache_pool, &p->cache_cursor, &p->cache_recs,
+                    &p->cache_cnt, &p->cache_off, &p->cache_w, &p->cache_xy, &p->cache_ranges,
+                    &p->cache_chunks, &p->cache_multi, &p->cache_scratch, &p->cache_counters};
   for (DevBuf *b : bufs) b->release();
 }
 
