@@ -60,14 +60,14 @@ METRIC = "Gaussian-views/sec motion-fit"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
 # our kernels per frame incl. CUB passes (profiles/r02_launches_cfg2.txt: 99 per 3 frames); the
-# K3 split (touched list + scan + compact fits + statuses; chosen from 8 M gvs on when no
-# per-view motions are requested, as here: cfg4, cfg5) adds 5
+# K3 split (touched list + scan + compact fits writing the statuses; chosen from 8 M gvs on when
+# no per-view motions are requested, as here: cfg4, cfg5) adds 4
 LAUNCHES_PER_STEP = 33
-LAUNCHES_K3_SPLIT = 5
-# clip mode with the contribution cache (profiles/r02_clip_launches_cfg{4,5}.txt: 222 launches
-# for two builds + 16 frames): binning + cache build 39, each cached frame 9
+LAUNCHES_K3_SPLIT = 4
+# clip mode with the contribution cache (profiles/r02_clip_launches_cfg{4,5}.txt: 206 launches
+# for two builds + 16 frames): binning + cache build 39, each cached frame 8
 LAUNCHES_CACHE_BUILD = 39
-LAUNCHES_CACHED_FRAME = 9
+LAUNCHES_CACHED_FRAME = 8
 
 
 def launches_per_step(n, nv):

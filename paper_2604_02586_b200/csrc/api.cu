@@ -634,8 +634,9 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
 
   const bool cached = p->cache_valid;
   // no motions requested and K3's fits compact (cache or touched list): K4 reads the fits in
-  // place and only the statuses are written densely (the per-view motions are intermediates of
-  // compensate_frame, pipeline.py:117-124; FrameResult does not carry them)
+  // place and only the statuses are written densely, by the fit kernels themselves over an
+  // UNSOLVABLE fill (the per-view motions are intermediates of compensate_frame,
+  // pipeline.py:117-124; FrameResult does not carry them)
   bool compact = false;
   if (cached) {
     compact = !motions && updates;
@@ -643,16 +644,20 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
     // contributions (no rasterization, no partials); list, ranks and ranges set by ts_frame_cache
     uint32_t *list = ptr<uint32_t>(p->k3_list);
     cudaEvent_t e3 = p->mark_begin(s);
+    // compact: the fit kernels write the listed gvs' statuses over an UNSOLVABLE fill
+    if (compact) TS_CUDA_TRY(cudaMemsetAsync(m.status, TS_STATUS_UNSOLVABLE, (size_t)NV, s));
     TS_CUDA_TRY(launch_k23_cached(p->cache_chunks.p, ptr<uint32_t>(p->cache_counters),
                                   p->cache_chunk_bound, p->cache_multi.p, p->cache_multi_bound,
                                   list, ptr<int16_t>(p->bbox), n, p->W, p->H,
                                   ptr<double>(p->cache_w), ptr<uint32_t>(p->cache_xy),
                                   track_target, track_dtype, track_valid, p->cfg, p->k3_fits.p,
-                                  ptr<double>(p->cache_scratch), s));
+                                  ptr<double>(p->cache_scratch), s,
+                                  compact ? m.status : nullptr));
     p->mark_end(ST_RASTER, e3, s);
     cudaEvent_t e4 = p->mark_begin(s);
-    launch_k3_merge(ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, NV, m, s,
-                    compact);
+    if (!compact)
+      launch_k3_merge(ptr<uint8_t>(p->touched), ptr<uint32_t>(p->k3_rank), p->k3_fits.p, NV, m,
+                      s);
     TS_CUDA_TRY(cudaGetLastError());
     p->mark_end(ST_SOLVE, e4, s);
   } else {

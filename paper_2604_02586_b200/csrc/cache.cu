@@ -106,7 +106,7 @@ struct __align__(16) CacheChunk {
   uint32_t beg, end;
   uint32_t part;  // KC_WHOLE: the gv's only chunk (solved in place); else its scratch slot
   int32_t ax, ay;  // the gv's anchor (integer bbox centre, as K2/K3)
-  uint32_t view, pad;
+  uint32_t view, gv;
 };
 constexpr uint32_t KC_WHOLE = 0xFFFFFFFFu;
 #ifndef TS_KC_CHUNK  // build-time overrides for variant experiments (tools/r2_libab.sh)
@@ -165,7 +165,7 @@ __global__ void cache_chunk_fill(const uint32_t *__restrict__ list,
       const uint32_t b = r.x + c * KC_CHUNK;
       chunks[c0 + c] = CacheChunk{i, b, min(b + (uint32_t)KC_CHUNK, r.y),
                                   part == KC_WHOLE ? KC_WHOLE : part + c, ax, ay,
-                                  (uint32_t)(gv / n), 0u};
+                                  (uint32_t)(gv / n), gv};
     }
   }
 }
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(KC_WARPS * 32, TS_KC_MIN_BLOCKS) k23_cached(
     const double *__restrict__ cw, const uint32_t *__restrict__ cxy,
     const TrackT *__restrict__ tgt, const uint8_t *__restrict__ val, double static_lim,
     double det_floor, int min_pixels, double min_weight, GvMotion *__restrict__ fits,
-    double *__restrict__ scratch) {
+    double *__restrict__ scratch, int8_t *__restrict__ status_out) {
   __shared__ double stage[KC_WARPS][32][KC_STAGE];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / KC_LANES, gl = lane % KC_LANES;
@@ -284,8 +284,10 @@ __global__ void __launch_bounds__(KC_WARPS * 32, TS_KC_MIN_BLOCKS) k23_cached(
         for (int q = 0; q < TS_NMOM; q++) m[q] = st[q];
         const uint32_t cnt = (uint32_t)__double2loint(st[TS_NMOM]);
         const uint32_t scnt = (uint32_t)__double2hiint(st[TS_NMOM]);
-        fits[mine.i] =
+        const GvMotion f =
             solve_moments(m, cnt, scnt, mine.ax, mine.ay, det_floor, min_pixels, min_weight);
+        fits[mine.i] = f;
+        if (status_out) status_out[mine.gv] = f.status;
       } else {
         double *dst = scratch + (size_t)mine.part * KC_STAGE;
 #pragma unroll
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(256) k23_cached_multi(
     const MultiGv *__restrict__ multi, const uint32_t *__restrict__ counters,
     const uint32_t *__restrict__ list, const int16_t *__restrict__ bbox,
     const double *__restrict__ scratch, double det_floor, int min_pixels, double min_weight,
-    GvMotion *__restrict__ fits) {
+    GvMotion *__restrict__ fits, int8_t *__restrict__ status_out) {
   const int lane = threadIdx.x & 31;
   const uint32_t nm = counters[2];
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -327,8 +329,11 @@ __global__ void __launch_bounds__(256) k23_cached_multi(
     }
     if (lane == 0) {
       int ax, ay;
-      gv_anchor(bbox, list[g.i], ax, ay);
-      fits[g.i] = solve_moments(m, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
+      const uint32_t gv = list[g.i];
+      gv_anchor(bbox, gv, ax, ay);
+      const GvMotion f = solve_moments(m, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
+      fits[g.i] = f;
+      if (status_out) status_out[gv] = f.status;
     }
   }
 }
@@ -391,7 +396,7 @@ cudaError_t launch_k23_cached(const void *chunks, const uint32_t *counters, uint
                               const int16_t *bbox, int64_t n, int W, int H, const double *cw,
                               const uint32_t *cxy, const void *track_target, int track_dtype,
                               const uint8_t *track_valid, const ts_config &cfg, void *fits,
-                              double *scratch, cudaStream_t s) {
+                              double *scratch, cudaStream_t s, int8_t *status_out) {
   if (!chunk_bound) return cudaSuccess;
   const double lim = static_sq_limit(cfg.static_threshold_px);
   int per_sm = 0;
@@ -406,17 +411,17 @@ cudaError_t launch_k23_cached(const void *chunks, const uint32_t *counters, uint
     k23_cached<float><<<grid_for((const void *)k23_cached<float>), KC_WARPS * 32, 0, s>>>(
         ch, counters, list, bbox, n, W, H, cw, cxy,
         reinterpret_cast<const float *>(track_target), track_valid, lim, cfg.det_floor,
-        cfg.min_pixels, cfg.min_weight, f, scratch);
+        cfg.min_pixels, cfg.min_weight, f, scratch, status_out);
   else
     k23_cached<double><<<grid_for((const void *)k23_cached<double>), KC_WARPS * 32, 0, s>>>(
         ch, counters, list, bbox, n, W, H, cw, cxy,
         reinterpret_cast<const double *>(track_target), track_valid, lim, cfg.det_floor,
-        cfg.min_pixels, cfg.min_weight, f, scratch);
+        cfg.min_pixels, cfg.min_weight, f, scratch, status_out);
   if (multi_bound) {
     const unsigned g2 = (unsigned)std::min<int64_t>((multi_bound + 7) / 8, sm_grid(8));
     k23_cached_multi<<<g2, 256, 0, s>>>(reinterpret_cast<const MultiGv *>(multi), counters, list,
                                         bbox, scratch, cfg.det_floor, cfg.min_pixels,
-                                        cfg.min_weight, f);
+                                        cfg.min_weight, f, status_out);
   }
   return cudaGetLastError();
 }

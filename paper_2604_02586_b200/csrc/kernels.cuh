@@ -79,10 +79,9 @@ cudaError_t launch_k23_cached(const void *chunks, const uint32_t *counters, uint
                               const int16_t *bbox, int64_t n, int W, int H, const double *cw,
                               const uint32_t *cxy, const void *track_target, int track_dtype,
                               const uint8_t *track_valid, const ts_config &cfg, void *fits,
-                              double *scratch, cudaStream_t s);
-// status_only: only m.status is written (K4 then reads the compact fits)
+                              double *scratch, cudaStream_t s, int8_t *status_out = nullptr);
 void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
-                     int64_t nv_total, ts_motions m, cudaStream_t s, bool status_only = false);
+                     int64_t nv_total, ts_motions m, cudaStream_t s);
 size_t k2_schedule_bytes(int n_tiles);  // workspace of the longest-first K2 schedule
 bool k2_writes_touched();  // the accumulate kernel in use marks per-gv touched bytes
 

@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
     const Partial *__restrict__ partial, const uint8_t *__restrict__ flag,
     const uint32_t *__restrict__ inst_base, const int16_t *__restrict__ bbox,
     const uint32_t *__restrict__ list, const uint32_t *__restrict__ n_list, double det_floor,
-    int min_pixels, double min_weight, GvMotion *__restrict__ fits) {
+    int min_pixels, double min_weight, GvMotion *__restrict__ fits,
+    int8_t *__restrict__ status_out) {
   const int lane = threadIdx.x & 31;
   const uint32_t nl = *n_list;
   // grid-stride over the device-side count (the grid is sized for the SMs, not the worst case)
@@ -153,8 +154,11 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
     ax = ((int)bb.x + (int)bb.y) >> 1;
     ay = ((int)bb.z + (int)bb.w) >> 1;
   }
-  if (valid && !big)
-    fits[i] = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels, min_weight);
+  if (valid && !big) {
+    const GvMotion f = solve_gv(partial, flag, sb, nq, ax, ay, det_floor, min_pixels, min_weight);
+    fits[i] = f;
+    if (status_out) status_out[gv] = f.status;  // compact mode: the dense statuses directly
+  }
   uint32_t bigmask = __ballot_sync(0xffffffffu, valid && big);
   while (bigmask) {
     const int j = __ffs(bigmask) - 1;
@@ -173,8 +177,11 @@ __global__ void __launch_bounds__(256, TS_K3_MIN_BLOCKS) k3_solve_list(
       cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
       scnt += __shfl_xor_sync(0xffffffffu, scnt, d);
     }
-    if (lane == j)
-      fits[i] = solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
+    if (lane == j) {
+      const GvMotion f = solve_moments(mom, cnt, scnt, ax, ay, det_floor, min_pixels, min_weight);
+      fits[i] = f;
+      if (status_out) status_out[gv] = f.status;
+    }
   }
   }
 }
@@ -273,24 +280,9 @@ __global__ void k_accumulate_segments(int64_t n, const uint32_t *__restrict__ se
 
 size_t k3_fit_bytes() { return sizeof(GvMotion); }
 
-// The statuses alone (the compact fits stay where they are for K4): 2 bytes per gv.
-__global__ void __launch_bounds__(256) k3_merge_status(const uint8_t *__restrict__ touched,
-                                                       const uint32_t *__restrict__ rank,
-                                                       const GvMotion *__restrict__ fits,
-                                                       int64_t NV, int8_t *__restrict__ status) {
-  const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gv >= NV) return;
-  status[gv] = touched[gv] ? fits[rank[gv]].status : (int8_t)TS_STATUS_UNSOLVABLE;
-}
-
 void launch_k3_merge(const uint8_t *touched, const uint32_t *rank, const void *fits,
-                     int64_t nv_total, ts_motions m, cudaStream_t s, bool status_only) {
+                     int64_t nv_total, ts_motions m, cudaStream_t s) {
   if (!nv_total) return;
-  if (status_only) {
-    k3_merge_status<<<blocks(nv_total, 256), 256, 0, s>>>(
-        touched, rank, reinterpret_cast<const GvMotion *>(fits), nv_total, m.status);
-    return;
-  }
   k3_merge<<<blocks(nv_total, 256), 256, 0, s>>>(touched, rank,
                                                  reinterpret_cast<const GvMotion *>(fits),
                                                  nv_total, m);
@@ -313,9 +305,13 @@ void launch_k3_solve(const Partial *partial, const uint8_t *flag, const uint32_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(blocks(nv_total, 256), (int64_t)sms * 8);
   GvMotion *f = reinterpret_cast<GvMotion *>(fits);
+  // status_only: the solve writes the statuses of the listed gvs over an UNSOLVABLE fill (K4
+  // reads the rest from the compact fits); otherwise the merge writes every dense motion
+  if (status_only) cudaMemsetAsync(m.status, TS_STATUS_UNSOLVABLE, (size_t)nv_total, s);
   k3_solve_list<<<(unsigned)grid, 256, 0, s>>>(partial, flag, inst_base, bbox, list, n_list,
-                                               cfg.det_floor, cfg.min_pixels, cfg.min_weight, f);
-  launch_k3_merge(touched, rank, f, nv_total, m, s, status_only);
+                                               cfg.det_floor, cfg.min_pixels, cfg.min_weight, f,
+                                               status_only ? m.status : nullptr);
+  if (!status_only) launch_k3_merge(touched, rank, f, nv_total, m, s);
 }
 
 void launch_solve_abs(const double *v1, const double *v2, const double *wsum, const int64_t *cnt,
