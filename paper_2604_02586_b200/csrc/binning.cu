@@ -23,7 +23,10 @@
 
 namespace ts {
 
-__global__ void __launch_bounds__(128) k1_project(const double *__restrict__ G, int64_t n,
+#ifndef TS_K1_MIN_BLOCKS
+#define TS_K1_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(128, TS_K1_MIN_BLOCKS) k1_project(const double *__restrict__ G, int64_t n,
                                                   const ts_camera *__restrict__ cams, int V,
                                                   RasterRec *__restrict__ rec,
                                                   uint32_t *__restrict__ drange,
