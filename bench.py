@@ -60,8 +60,8 @@ METRIC = "Gaussian-views/sec motion-fit"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK = 6650.0
 # our kernels per frame incl. CUB passes (profiles/r02_launches_cfg2.txt: 99 per 3 frames); the
-# K3 split (touched list + scan + compact fits writing the statuses; chosen from 8 M gvs on when
-# no per-view motions are requested, as here: cfg4, cfg5) adds 4
+# K3 split (touched list + scan + compact fits writing the statuses; chosen from 4 M gvs on when
+# no per-view motions are requested, as here: cfg2-cfg5) adds 4
 LAUNCHES_PER_STEP = 33
 LAUNCHES_K3_SPLIT = 4
 # clip mode with the contribution cache (profiles/r02_clip_launches_cfg{4,5}.txt: 206 launches
@@ -71,8 +71,8 @@ LAUNCHES_CACHED_FRAME = 8
 
 
 def launches_per_step(n, nv):
-    # the bench asks for no per-view motions: K3 splits from 8 M gvs on (api.cu)
-    return LAUNCHES_PER_STEP + (LAUNCHES_K3_SPLIT if n * nv >= (8 << 20) else 0)
+    # the bench asks for no per-view motions: K3 splits from 4 M gvs on (api.cu)
+    return LAUNCHES_PER_STEP + (LAUNCHES_K3_SPLIT if n * nv >= (4 << 20) else 0)
 
 
 def log(*a):

@@ -667,10 +667,10 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   // the single pass when many do (cfg2: ~40%, 0.44 vs 0.50 ms).  The plan keeps the touched
   // fraction of its previous frame (copied back asynchronously; read after the next binning's
   // stream synchronisation); the first frame splits from 16 M gvs on.  Without requested motions
-  // the split also spares the dense motion stores (K4 reads the compact fits), so it is taken
-  // from 8 M gvs on and kept up to half the gvs touched (cfg4, 10 M gvs: K3 0.61 -> 0.48 ms,
-  // step 4.19 -> 4.03 ms; cfg2 / cfg3 stay single pass: 3.64 vs 3.67, 2.60 vs 2.61 ms).
-  // TS_K3_SPLIT=0/1 forces.
+  // the split also spares the dense motion stores (K4 reads the compact fits, statuses written
+  // over an UNSOLVABLE fill), so it is taken from 4 M gvs on and kept up to half the gvs touched
+  // (cfg4, 10 M gvs: K3 0.61 -> 0.48 ms, step 4.19 -> 4.03 ms; cfg2, 6 M gvs, 40% touched:
+  // step 3.64 -> 3.59 ms; cfg3 2.60 -> 2.59 ms).  TS_K3_SPLIT=0/1 forces.
   static const char *force = getenv("TS_K3_SPLIT");
   const bool lean = !motions && updates;
   bool split;
@@ -681,7 +681,7 @@ int ts_frame_compensate(ts_plan *p, const void *track_target, int32_t track_dtyp
   } else if (p->k3_last_nv == NV) {
     split = false;  // sticky: the single pass does not measure the touched fraction
   } else {
-    split = NV >= (int64_t)(lean ? 8 : 16) << 20;
+    split = NV >= (int64_t)(lean ? 4 : 16) << 20;
   }
   p->k3_last_nv = NV;
   p->k3_last_split = split;

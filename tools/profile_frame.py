@@ -23,6 +23,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--frames", type=int, default=3)
+    ap.add_argument("--lean", action="store_true",
+                    help="updates only, no per-view motions (the bench's outputs)")
     args = ap.parse_args()
     c = bench.CONFIGS[args.config]
     scene, tracks = bench.make_inputs(args.config, c["gap"] + 1)
@@ -36,7 +38,7 @@ def main():
         t0 = time.perf_counter()
         torch.cuda.nvtx.range_push("frame")
         eng.bin(g, scene.cameras)
-        out = eng.compensate(tgt, val, out)
+        out = eng.compensate(tgt, val, out, motions=not args.lean)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         print(f"frame {i}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, "
