@@ -52,6 +52,10 @@ constexpr int64_t K1_TIE_RUN_MAX_HOST = 64;  // binning.cu K1_TIE_RUN_MAX
                            // cfg5 2.27 -> 2.75 ms (3M Gaussians per view in 2^20 levels: tie runs)
 #endif
 
+#ifndef TS_K1_DEPTH_BITS_MAX
+#define TS_K1_DEPTH_BITS_MAX 26
+#endif
+
 int bits_for(uint64_t x) {  // number of bits needed to represent values < x
   int b = 0;
   while (b < 64 && (1ull << b) < x) b++;
@@ -364,8 +368,9 @@ int frame_bin(ts_plan *p, const double *G, int64_t n, const ts_camera *cams, int
 
   cudaEvent_t e0 = p->mark_begin(s);
   ENSURE(p->drange, 4 * (K1_RECT_OFFSET + 4 * 64));
-  // depth key: view bits + quantised depth (at most 2^26 levels), TS_K1_KEY_BITS in all
-  const int dbits = std::min(26, TS_K1_KEY_BITS - bits_for((uint64_t)V));
+  // depth key: view bits + quantised depth (at most 2^TS_K1_DEPTH_BITS_MAX levels),
+  // TS_K1_KEY_BITS in all
+  const int dbits = std::min(TS_K1_DEPTH_BITS_MAX, TS_K1_KEY_BITS - bits_for((uint64_t)V));
   launch_k1_project(G, n, ptr<ts_camera>(p->cams), V, dbits, ptr<RasterRec>(p->rec),
                     ptr<uint32_t>(p->drange), ptr<uint32_t>(p->dkey),
                     ptr<uint32_t>(p->dval), ptr<double>(p->depth64), ptr<uint32_t>(p->ntiles),

@@ -85,12 +85,10 @@ __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gv = (int64_t)v * n + g;
-    const double d = depth64[gv];
+    const double d = depth64[gv];  // -1 unless binned (status 3): no status read
     if (d > 0.0) {
       lo = min(lo, __float_as_uint(__double2float_rd(d)));
       hi = max(hi, __float_as_uint(__double2float_ru(d)));
-    }
-    if (status[gv] == 3) {
       const short4 b = reinterpret_cast<const short4 *>(bbox)[gv];  // x0 x1 y0 y1
       rx0 = min(rx0, (int)b.x);
       rx1 = max(rx1, (int)b.y);
@@ -154,13 +152,14 @@ __global__ void k1_depth_keys(const double *__restrict__ depth64,
   const uint32_t v = (uint32_t)(gv / n);
   const uint32_t sentinel = (1u << dbits) - 1u;
   uint32_t key = v << dbits;
-  if (status[gv] == 3) {
+  const double d = depth64[gv];  // -1 unless binned (status 3): no status read
+  if (d > 0.0) {
     const double dmin = (double)__uint_as_float(drange[2 * v]);
     const double dmax = (double)__uint_as_float(drange[2 * v + 1]);
     const double span = dmax - dmin;
     const double top = (double)(sentinel - 1u);
     const double scale = span > 0.0 ? top / span : 0.0;
-    const double qd = fmin(fmax((depth64[gv] - dmin) * scale, 0.0), top);
+    const double qd = fmin(fmax((d - dmin) * scale, 0.0), top);
     key |= (uint32_t)qd;
   } else {
     key |= sentinel;  // sorts after every binned Gaussian of the view, never emitted
