@@ -5,7 +5,7 @@
 // tile's Gaussian list by the same key, so every pixel of the tile sees its Gaussians in exactly
 // the reference order:
 //   1. k1_project: one thread per Gaussian, looping over the V cameras (the 88-byte Gaussian is
-//      read once): writes the 64-byte RasterRec, a 32-bit sort key (view << 26 | top 26 bits of
+//      read once): writes the 64-byte RasterRec, a 32-bit sort key (view << b | quantised depth, b = min(28, 32 - view bits) of
 //      the positive f32 depth) and the tile count of its bbox.
 //   2. CUB radix sort by that key (31 bits at V=20, 4 passes).  Rounding to f32 and dropping low
 //      mantissa bits are monotone, so the order is right except inside runs of equal keys;
@@ -139,9 +139,9 @@ __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__
   }
 }
 
-// 32-bit depth keys v << 26 | q, q = floor((d - dmin) * (2^26 - 2) / (dmax - dmin)) over the
+// 32-bit depth keys v << b | q, q = floor((d - dmin) * (2^b - 2) / (dmax - dmin)) over the
 // view's depth range: monotone in d (so the radix sort plus the exact tie repair below yields
-// the reference's (depth, gid) order) and resolving ~2^26 levels per view instead of the 18
+// the reference's (depth, gid) order) and resolving 2^27-2^28 levels per view (b = min(28, 32 - view bits)) instead of the 18
 // mantissa bits a truncated float key keeps (far fewer ties to repair).
 __global__ void k1_depth_keys(const double *__restrict__ depth64,
                               const int8_t *__restrict__ status,
