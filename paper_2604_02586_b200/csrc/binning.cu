@@ -5,11 +5,13 @@
 // tile's Gaussian list by the same key, so every pixel of the tile sees its Gaussians in exactly
 // the reference order:
 //   1. k1_project: one thread per Gaussian, looping over the V cameras (the 88-byte Gaussian is
-//      read once): writes the 64-byte RasterRec, a 32-bit sort key (view << b | quantised depth, b = min(28, 32 - view bits) of
-//      the positive f32 depth) and the tile count of its bbox.
-//   2. CUB radix sort by that key (31 bits at V=20, 4 passes).  Rounding to f32 and dropping low
-//      mantissa bits are monotone, so the order is right except inside runs of equal keys;
-//      k1_fix_ties re-sorts those (short) runs by the exact (f64 depth, gid) key.
+//      read once): writes the 64-byte RasterRec, the exact f64 depth (-1 unless binned), the
+//      bbox and its tile count.  k1_depth_range reduces each view's depth range and
+//      k1_depth_keys forms the 32-bit key view << b | quantised depth (b = min(28, 32 - view
+//      bits)).
+//   2. CUB radix sort by that key (4 passes).  The quantisation is monotone, so the order is
+//      right except inside runs of equal keys; k1_fix_ties re-sorts those runs by the exact
+//      (f64 depth, gid) key.
 //   3. k1_emit writes one (tile, gv) instance per covered tile in that depth order (views are
 //      contiguous: the view is the top field of the depth key); a stable CUB radix sort on the
 //      tile id WITHIN the view (13 bits at 1352x1014: two onesweep passes instead of three for
