@@ -6,9 +6,9 @@
 // the reference order:
 //   1. k1_project: one thread per Gaussian, looping over the V cameras (the 88-byte Gaussian is
 //      read once): writes the 64-byte RasterRec, the exact f64 depth (-1 unless binned), the
-//      bbox and its tile count.  k1_depth_range reduces each view's depth range and
-//      k1_depth_keys forms the 32-bit key view << b | quantised depth (b = min(28, 32 - view
-//      bits)).
+//      bbox, its tile count and the 32-bit key view << b | quantised depth (b = min(28, 32 -
+//      view bits)) over the view's depth range, which k1_depth_bounds reduced beforehand from
+//      the means; k1_bbox_union then reduces each view's union of binned bboxes.
 //   2. CUB radix sort by that key (4 passes).  The quantisation is monotone, so the order is
 //      right except inside runs of equal keys; k1_fix_ties re-sorts those runs by the exact
 //      (f64 depth, gid) key.
@@ -25,6 +25,136 @@
 
 namespace ts {
 
+// Quantisation of a view's depths into the key (k1_depth_keys / k1_project): (dmin, scale).
+__device__ __forceinline__ double2 depth_quant(const uint32_t *drange, int v, int dbits) {
+  const double dmin = (double)__uint_as_float(drange[2 * v]);
+  const double dmax = (double)__uint_as_float(drange[2 * v + 1]);
+  const double span = dmax - dmin;
+  const double top = (double)((1u << dbits) - 2u);
+  return make_double2(dmin, span > 0.0 ? top / span : 0.0);
+}
+// v << dbits | q for a binned depth d > 0 (clamped into [0, top]: monotone in d whatever the
+// range), the sentinel 2^dbits - 1 (after every binned gv of the view, never emitted) otherwise
+__device__ __forceinline__ uint32_t depth_key(double d, double2 q, uint32_t v, int dbits) {
+  const uint32_t sentinel = (1u << dbits) - 1u;
+  uint32_t key = v << dbits;
+  if (d > 0.0) {
+    const double top = (double)(sentinel - 1u);
+    key |= (uint32_t)fmin(fmax((d - q.x) * q.y, 0.0), top);
+  } else {
+    key |= sentinel;
+  }
+  return key;
+}
+
+// Per-view bounds of the in-front depths (TS_K1_FUSED_KEYS): the camera-space z of project()
+// (same dot3 + add, so the same bits) for every Gaussian in front of the camera -- a superset of
+// the binned ones, so the range holds every binned depth (a wider range costs key resolution,
+// never order: the exact tie repair follows the sort).  Reads only the means, so k1_project
+// can write the keys itself (no k1_depth_keys pass over the depths).
+__global__ void __launch_bounds__(256) k1_depth_bounds(const double *__restrict__ G, int64_t n,
+                                                       const ts_camera *__restrict__ cams, int V,
+                                                       uint32_t *__restrict__ drange) {
+  __shared__ double s_c[64][4];  // R row 2 and t[2] of each camera
+  __shared__ uint32_t s_lo[64], s_hi[64];
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    s_c[i][0] = cams[i].R[6];
+    s_c[i][1] = cams[i].R[7];
+    s_c[i][2] = cams[i].R[8];
+    s_c[i][3] = cams[i].t[2];
+    s_lo[i] = 0xFFFFFFFFu;
+    s_hi[i] = 0u;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = b + threadIdx.x;
+    const bool ok = g < n;
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+    if (ok) {
+      m0 = G[11 * g];
+      m1 = G[11 * g + 1];
+      m2 = G[11 * g + 2];
+    }
+    for (int v = 0; v < V; v++) {
+      uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+      const double z = add(dot3(m0, m1, m2, s_c[v][0], s_c[v][1], s_c[v][2]), s_c[v][3]);
+      if (ok && z > TS_DEPTH_CUTOFF) {
+        lo = __float_as_uint(__double2float_rd(z));
+        hi = __float_as_uint(__double2float_ru(z));
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+      }
+      if (lane == 0 && hi != 0u) {
+        atomicMin(&s_lo[v], lo);
+        atomicMax(&s_hi[v], hi);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    if (s_hi[i] != 0u) {
+      atomicMin(&drange[2 * i], s_lo[i]);
+      atomicMax(&drange[2 * i + 1], s_hi[i]);
+    }
+  }
+}
+
+// Per-view union of the binned bboxes only (TS_K1_FUSED_KEYS; the sentinel bbox of a
+// non-binned gv has x1 < x0).
+__global__ void __launch_bounds__(256) k1_bbox_union(const int16_t *__restrict__ bbox, int64_t n,
+                                                     uint32_t *__restrict__ drange) {
+  const int v = blockIdx.y;
+  int rx0 = 0x7FFFFFFF, ry0 = 0x7FFFFFFF, rx1 = -1, ry1 = -1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const short4 b = reinterpret_cast<const short4 *>(bbox)[(int64_t)v * n + g];  // x0 x1 y0 y1
+    if (b.x <= b.y) {
+      rx0 = min(rx0, (int)b.x);
+      rx1 = max(rx1, (int)b.y);
+      ry0 = min(ry0, (int)b.z);
+      ry1 = max(ry1, (int)b.w);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    rx0 = min(rx0, __shfl_xor_sync(0xffffffffu, rx0, d));
+    ry0 = min(ry0, __shfl_xor_sync(0xffffffffu, ry0, d));
+    rx1 = max(rx1, __shfl_xor_sync(0xffffffffu, rx1, d));
+    ry1 = max(ry1, __shfl_xor_sync(0xffffffffu, ry1, d));
+  }
+  __shared__ int s_r[4][8];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_r[0][w] = rx0;
+    s_r[1][w] = ry0;
+    s_r[2][w] = rx1;
+    s_r[3][w] = ry1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < nw; k++) {
+      rx0 = min(rx0, s_r[0][k]);
+      ry0 = min(ry0, s_r[1][k]);
+      rx1 = max(rx1, s_r[2][k]);
+      ry1 = max(ry1, s_r[3][k]);
+    }
+    if (rx1 >= 0) {
+      int *r = reinterpret_cast<int *>(drange + K1_RECT_OFFSET) + 4 * v;
+      atomicMin(r, rx0);
+      atomicMin(r + 1, ry0);
+      atomicMax(r + 2, rx1);
+      atomicMax(r + 3, ry1);
+    }
+  }
+}
+
+#ifndef TS_K1_FUSED_KEYS
+#define TS_K1_FUSED_KEYS 1  // 0: k1_depth_range + k1_depth_keys after k1_project (K1 stage cfg5 1.65 vs 1.54 ms)
+#endif
 #ifndef TS_K1_MIN_BLOCKS
 #define TS_K1_MIN_BLOCKS 1
 #endif
@@ -36,9 +166,18 @@ __global__ void __launch_bounds__(128, TS_K1_MIN_BLOCKS) k1_project(const double
                                                   double *__restrict__ depth64,
                                                   uint32_t *__restrict__ ntiles,
                                                   int8_t *__restrict__ status,
-                                                  int16_t *__restrict__ bbox) {
+                                                  int16_t *__restrict__ bbox,
+                                                  uint32_t *__restrict__ dkey, int dbits) {
   extern __shared__ ts_camera s_cam[];
-  for (int i = threadIdx.x; i < V; i += blockDim.x) s_cam[i] = cams[i];
+  double *s_q = reinterpret_cast<double *>(s_cam + V);  // (dmin, scale) per view (dkey)
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    s_cam[i] = cams[i];
+    if (dkey) {
+      const double2 q = depth_quant(drange, i, dbits);
+      s_q[2 * i] = q.x;
+      s_q[2 * i + 1] = q.y;
+    }
+  }
   __syncthreads();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n) return;
@@ -67,6 +206,9 @@ __global__ void __launch_bounds__(128, TS_K1_MIN_BLOCKS) k1_project(const double
     }
     dval[gv] = (uint32_t)gv;
     depth64[gv] = st == 3 ? p.depth : -1.0;  // -1: not binned (excluded from the depth range)
+    if (dkey)
+      dkey[gv] = depth_key(st == 3 ? p.depth : -1.0, make_double2(s_q[2 * v], s_q[2 * v + 1]),
+                           (uint32_t)v, dbits);
     ntiles[gv] = nt;
     reinterpret_cast<short4 *>(bbox)[gv] = make_short4(bb[0], bb[1], bb[2], bb[3]);
   }
@@ -146,27 +288,13 @@ __global__ void __launch_bounds__(256) k1_depth_range(const double *__restrict__
 // the reference's (depth, gid) order) and resolving 2^27-2^28 levels per view (b = min(28, 32 - view bits)) instead of the 18
 // mantissa bits a truncated float key keeps (far fewer ties to repair).
 __global__ void k1_depth_keys(const double *__restrict__ depth64,
-                              const int8_t *__restrict__ status,
                               const uint32_t *__restrict__ drange, int64_t n, int V, int dbits,
                               uint32_t *__restrict__ dkey) {
   const int64_t gv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gv >= n * V) return;
-  const uint32_t v = (uint32_t)(gv / n);
-  const uint32_t sentinel = (1u << dbits) - 1u;
-  uint32_t key = v << dbits;
-  const double d = depth64[gv];  // -1 unless binned (status 3): no status read
-  if (d > 0.0) {
-    const double dmin = (double)__uint_as_float(drange[2 * v]);
-    const double dmax = (double)__uint_as_float(drange[2 * v + 1]);
-    const double span = dmax - dmin;
-    const double top = (double)(sentinel - 1u);
-    const double scale = span > 0.0 ? top / span : 0.0;
-    const double qd = fmin(fmax((d - dmin) * scale, 0.0), top);
-    key |= (uint32_t)qd;
-  } else {
-    key |= sentinel;  // sorts after every binned Gaussian of the view, never emitted
-  }
-  dkey[gv] = key;
+  const int v = (int)(gv / n);
+  // -1 unless binned (status 3): no status read
+  dkey[gv] = depth_key(depth64[gv], depth_quant(drange, v, dbits), (uint32_t)v, dbits);
 }
 
 // Re-sort runs of equal (view, quantised depth) keys by the exact (f64 depth, gid) key.  Runs
@@ -337,13 +465,23 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
                        cudaStream_t s) {
   if (n == 0) return;
   k1_range_init<<<1, 64, 0, s>>>(drange, V);
-  k1_project<<<blocks(n, 128), 128, sizeof(ts_camera) * V, s>>>(G, n, cams, V, rec, drange, dval,
-                                                                  depth64, ntiles, status, bbox);
   // enough blocks per view that each thread reads ~8 gvs (16 per view was latency-bound at
   // cfg5: 0.41 ms for 48 M gvs)
   const int per_view = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (n + 2047) / 2048));
-  k1_depth_range<<<dim3(per_view, V), 256, 0, s>>>(depth64, status, bbox, n, drange);
-  k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, status, drange, n, V, dbits, dkey);
+  const size_t smem = (sizeof(ts_camera) + 2 * sizeof(double)) * V;
+  if (TS_K1_FUSED_KEYS) {
+    // depth bounds from the means first, keys written by k1_project, bbox union afterwards
+    k1_depth_bounds<<<(unsigned)std::min<int64_t>(blocks(n, 256), 148 * 8), 256, 0, s>>>(
+        G, n, cams, V, drange);
+    k1_project<<<blocks(n, 128), 128, smem, s>>>(G, n, cams, V, rec, drange, dval, depth64,
+                                                 ntiles, status, bbox, dkey, dbits);
+    k1_bbox_union<<<dim3(per_view, V), 256, 0, s>>>(bbox, n, drange);
+  } else {
+    k1_project<<<blocks(n, 128), 128, smem, s>>>(G, n, cams, V, rec, drange, dval, depth64,
+                                                 ntiles, status, bbox, nullptr, dbits);
+    k1_depth_range<<<dim3(per_view, V), 256, 0, s>>>(depth64, status, bbox, n, drange);
+    k1_depth_keys<<<blocks(n * V, 256), 256, 0, s>>>(depth64, drange, n, V, dbits, dkey);
+  }
 }
 void launch_k1_fix_ties(const uint32_t *key, uint32_t *val, const double *depth64, int64_t M,
                         int dbits, uint32_t *long_runs, uint32_t long_cap, cudaStream_t s) {
