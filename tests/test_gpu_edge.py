@@ -177,6 +177,40 @@ def test_long_depth_tie_runs_bit_exact():
     np.testing.assert_array_equal(b["inst_gv"][idx].astype(np.int64), ref["inst_gid"])
 
 
+def test_far_offscreen_gaussians_widen_depth_range_bit_exact():
+    """K1's key range comes from every in-front Gaussian (k1_depth_bounds), a superset of the
+    binned ones: far-away Gaussians off the image (in front, never binned) stretch the range by
+    six orders of magnitude, so most binned depths share quantised keys and the order rests on
+    the exact tie repair.  Binning must still equal the oracle bit for bit."""
+    import oracle
+    from paper_2604_02586_b200.engine import FrameEngine
+    rng = np.random.default_rng(5)
+    n_vis, n_far = 6000, 50
+    n = n_vis + n_far
+    g = np.zeros((n, 11))
+    g[:n_vis, 0] = rng.uniform(-2.0, 2.0, n_vis)
+    g[:n_vis, 1] = rng.uniform(-1.5, 1.5, n_vis)
+    g[:n_vis, 2] = rng.uniform(5.0, 5.0 + 1e-6, n_vis)  # a thin slab: ~50 key levels at most
+    g[n_vis:, 0] = rng.uniform(1e8, 2e8, n_far)          # far to the side: off the image
+    g[n_vis:, 2] = rng.uniform(1e6, 2e6, n_far)
+    q = rng.normal(size=(n, 4))
+    g[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    g[:, 7:10] = rng.uniform(0.004, 0.01, (n, 3))
+    g[:, 10] = 0.9
+    cam = np.zeros(18)
+    cam[[0, 4, 8]] = 1.0
+    cam[12:18] = [500.0, 500.0, 320.0, 240.0, 640, 480]
+    eng = FrameEngine().bin(g, cam[None])
+    b = eng.binning()
+    ref = oracle.bin_view(g, cam)
+    np.testing.assert_array_equal(b["status"], ref["status"])
+    assert (ref["status"][n_vis:] != 3).all() and (ref["status"][:n_vis] == 3).sum() > 1000
+    rng_ = b["tile_range"].astype(np.int64)
+    np.testing.assert_array_equal(rng_[:, 1] - rng_[:, 0], ref["tile_count"])
+    idx = gd.tile_order_index(rng_)
+    np.testing.assert_array_equal(b["inst_gv"][idx].astype(np.int64), ref["inst_gid"])
+
+
 def test_empty_frame(scene7):
     """No Gaussians (the reference returns empty lists): every stage handles N = 0."""
     from paper_2604_02586_b200.engine import FrameEngine
