@@ -47,6 +47,9 @@ __device__ __forceinline__ uint32_t depth_key(double d, double2 q, uint32_t v, i
   return key;
 }
 
+#ifndef K1_BOUNDS_PER_THREAD
+#define K1_BOUNDS_PER_THREAD 4
+#endif
 // Per-view bounds of the in-front depths (TS_K1_FUSED_KEYS): the camera-space z of project()
 // (same dot3 + add, so the same bits) for every Gaussian in front of the camera -- a superset of
 // the binned ones, so the range holds every binned depth (a wider range costs key resolution,
@@ -67,21 +70,31 @@ __global__ void __launch_bounds__(256) k1_depth_bounds(const double *__restrict_
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = b + threadIdx.x;
-    const bool ok = g < n;
-    double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-    if (ok) {
-      m0 = G[11 * g];
-      m1 = G[11 * g + 1];
-      m2 = G[11 * g + 2];
+  // each thread holds K1_BOUNDS_PER_THREAD means, so a view's warp reduction is paid once per
+  // that many Gaussians per lane
+  constexpr int PT = K1_BOUNDS_PER_THREAD;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * PT;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * PT; b < n; b += stride) {
+    double m[PT][3];
+    bool ok[PT];
+#pragma unroll
+    for (int k = 0; k < PT; k++) {
+      const int64_t g = b + (int64_t)k * blockDim.x + threadIdx.x;
+      ok[k] = g < n;
+      m[k][0] = ok[k] ? G[11 * g] : 0.0;
+      m[k][1] = ok[k] ? G[11 * g + 1] : 0.0;
+      m[k][2] = ok[k] ? G[11 * g + 2] : 0.0;
     }
     for (int v = 0; v < V; v++) {
       uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-      const double z = add(dot3(m0, m1, m2, s_c[v][0], s_c[v][1], s_c[v][2]), s_c[v][3]);
-      if (ok && z > TS_DEPTH_CUTOFF) {
-        lo = __float_as_uint(__double2float_rd(z));
-        hi = __float_as_uint(__double2float_ru(z));
+#pragma unroll
+      for (int k = 0; k < PT; k++) {
+        const double z = add(dot3(m[k][0], m[k][1], m[k][2], s_c[v][0], s_c[v][1], s_c[v][2]),
+                             s_c[v][3]);
+        if (ok[k] && z > TS_DEPTH_CUTOFF) {
+          lo = min(lo, __float_as_uint(__double2float_rd(z)));
+          hi = max(hi, __float_as_uint(__double2float_ru(z)));
+        }
       }
 #pragma unroll
       for (int d = 16; d > 0; d >>= 1) {
@@ -471,7 +484,8 @@ void launch_k1_project(const double *G, int64_t n, const ts_camera *cams, int V,
   const size_t smem = (sizeof(ts_camera) + 2 * sizeof(double)) * V;
   if (TS_K1_FUSED_KEYS) {
     // depth bounds from the means first, keys written by k1_project, bbox union afterwards
-    k1_depth_bounds<<<(unsigned)std::min<int64_t>(blocks(n, 256), 148 * 8), 256, 0, s>>>(
+    k1_depth_bounds<<<(unsigned)std::min<int64_t>(blocks(n, 256 * K1_BOUNDS_PER_THREAD), 148 * 8),
+                      256, 0, s>>>(
         G, n, cams, V, drange);
     k1_project<<<blocks(n, 128), 128, smem, s>>>(G, n, cams, V, rec, drange, dval, depth64,
                                                  ntiles, status, bbox, dkey, dbits);
